@@ -1,0 +1,60 @@
+"""ORACLE - TEST INFRASTRUCTURE ONLY.
+
+Alg. 1 Steps 4b-4c, written out as plain loops over the
+canonical task order (SURVEY.md §8 notation; reading 17):
+
+    E   = sum_{l,k} sum_{j} c_l^* c_k (Re + i Im)_{num(l,k,j)}     (Step 4b)
+    Psi = sum_{l,k}         c_l^* c_k (Re + i Im)_{den(l,k)}       (Step 4b)
+    C   = 1/2 - 1/2 * Re E / (n * Re Psi)                          (Step 4c)
+
+The real parts are used in C (reading 12); Re Psi <= 1e-12 is an error
+(reading 13).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+class DegenerateDenominator(ValueError):
+    pass
+
+
+def aggregate(terms: np.ndarray, coeffs, n: int, L: int, circuits=None):
+    """(E, Psi) from term expectations.
+
+    ``terms[i]`` is the value of circuit ``circuits[i]`` (default: all circuits in
+    canonical order c = 2t + part).
+    """
+    c = np.asarray(coeffs, dtype=np.complex128)
+    E = 0j
+    Psi = 0j
+    idx = range(len(terms)) if circuits is None else None
+    items = zip(idx, terms) if circuits is None else zip(circuits, terms)
+    for circ, val in items:
+        t, part = divmod(int(circ), 2)
+        s = t % (n + 1)
+        k = (t // (n + 1)) % L
+        l = t // ((n + 1) * L)
+        w = np.conj(c[l]) * c[k]
+        contrib = w * (val if part == 0 else 1j * val)
+        if s == 0:
+            Psi += contrib
+        else:
+            E += contrib
+    return complex(E), complex(Psi)
+
+
+def cost_from(E: complex, Psi: complex, n: int) -> float:
+    if Psi.real <= 1e-12:
+        raise DegenerateDenominator(f"Re Psi = {Psi.real} <= 1e-12")
+    return 0.5 - 0.5 * E.real / (n * Psi.real)
+
+
+def cost(terms: np.ndarray, coeffs, n: int, L: int):
+    E, Psi = aggregate(terms, coeffs, n, L)
+    return cost_from(E, Psi, n), E, Psi
+
+
+def coeffs_of(w) -> np.ndarray:
+    return np.array([c for c, _ in w.terms], dtype=np.complex128)
