@@ -1,0 +1,391 @@
+#!/usr/bin/env python3
+"""Benchmark of the D-VQLS hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3|cfg4|cfg1]
+                    [--batch KT] [--impl dvqls|reference] [--no-cpu-baseline]
+
+One *step* = one pass of the whole hot path (prefix
+V(theta)|0>, all 2(n+1)L^2 Hadamard-test circuits, weighted reduction,
+cross-rank allreduce, cost) for KT thetas.  Default workload: BASELINE config 3
+(n=10, L=64, d=10; 90,112 circuits per cost evaluation).  With N ranks each GPU
+evaluates a contiguous 1/N block of the circuits and one NCCL allreduce of
+4 doubles per theta combines them (strong scaling over a fixed workload).
+
+`value` = whole-job circuits/s with theta resident in HBM (device entry point
+dvqls_cost_dev), timed with CUDA events on the library's stream, L2 flushed
+(256 MiB write) before every step, max over ranks.  `e2e` = the same metric
+through the host-buffer C-ABI call dvqls_cost (theta H2D + result D2H inside).
+The oracle (oracle/, test infrastructure) is only executed for `cpu_baseline`
+(rank 0, N = 1) and for `--impl reference`.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from dvqls_inputs import configs  # noqa: E402
+
+CONFIGS = {"cfg1": configs.cfg1, "cfg3": configs.cfg3, "cfg4": configs.cfg4}
+METRIC = "Hadamard-test circuits/sec & cost evals/sec, 10q 90,112 circuits, 1/2/4/8 B200"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def fp64_ops_per_eval(w, circuits=None):
+    """Algorithmic FP64-pipe ops (DADD and DFMA count 1 each), SURVEY §8(d):
+    numerator circuit (4n+2)N (two n-stage FWHTs at 2N DADD/stage + 2N DFMA
+    readout), denominator 2N; uniform b."""
+    N = 1 << w.n
+    n1 = w.n + 1
+    c = np.arange(w.n_circuits) if circuits is None else circuits
+    s = (c // 2) % n1
+    num = int(np.count_nonzero(s))
+    den = c.size - num
+    return num * (4 * w.n + 2) * N + den * 2 * N
+
+
+def smem_bytes_per_eval(w, circuits=None):
+    """On-chip model bytes: numerator 96N, denominator 32N."""
+    N = 1 << w.n
+    c = np.arange(w.n_circuits) if circuits is None else circuits
+    s = (c // 2) % (w.n + 1)
+    num = int(np.count_nonzero(s))
+    return num * 96 * N + (c.size - num) * 32 * N
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", ",".join(map(str, self.gpus)), "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def traffic_from_profiles():
+    p = os.path.join(ROOT, "profiles", "hadamard_dram_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
+# ----------------------------------------------------------------------------------------------
+def cpu_baseline(w, theta, budget_s=12.0):
+    """Oracle (as it stands) on all host cores, bounded strided samples of the workload."""
+    from oracle import sim
+    cores = sim.hardware_threads()
+    out = {"kind": "oracle", "cores": cores, "unit": "circuits/s"}
+    res = {}
+    for mode, name in ((0, "faithful"), (1, "prefix_shared")):
+        n_probe = max(cores, 8)
+        idx = np.linspace(0, w.n_circuits - 1, n_probe).astype(np.int64)
+        t0 = time.perf_counter()
+        sim.workload_terms(w, theta, mode=mode, idx=idx, nthreads=cores)
+        dt = time.perf_counter() - t0
+        per = dt / n_probe
+        m = int(min(w.n_circuits, max(n_probe, budget_s / 2 / max(per, 1e-9))))
+        idx = np.linspace(0, w.n_circuits - 1, m).astype(np.int64)
+        t0 = time.perf_counter()
+        sim.workload_terms(w, theta, mode=mode, idx=idx, nthreads=cores)
+        dt = time.perf_counter() - t0
+        res[name] = (m / dt, m, dt)
+    out["value"] = res["faithful"][0]
+    out["prefix_shared_value"] = res["prefix_shared"][0]
+    out["sample"] = (f"{res['faithful'][1]} (faithful, {res['faithful'][2]:.1f} s) and {res['prefix_shared'][1]} "
+                     f"(prefix-shared, {res['prefix_shared'][2]:.1f} s) evenly strided circuits of {w.name}, "
+                     f"gate-by-gate C++ oracle, std::thread over {cores} host threads")
+    return out
+
+
+def run_reference(args, w):
+    """--impl reference: the oracle as the reference arm (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import sim
+    cores = sim.hardware_threads()
+    theta = w.theta0()
+    # size one step to ~3 s of faithful-mode work on all cores
+    n_probe = max(cores, 8)
+    idx = np.linspace(0, w.n_circuits - 1, n_probe).astype(np.int64)
+    t0 = time.perf_counter()
+    sim.workload_terms(w, theta, mode=0, idx=idx, nthreads=cores)
+    per = (time.perf_counter() - t0) / n_probe
+    m = int(min(w.n_circuits, max(n_probe, 3.0 / max(per, 1e-9))))
+    idx = np.linspace(0, w.n_circuits - 1, m).astype(np.int64)
+    for _ in range(args.warmup):
+        sim.workload_terms(w, theta, mode=0, idx=idx[: max(1, m // 10)], nthreads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sim.workload_terms(w, theta, mode=0, idx=idx, nthreads=cores)
+    dt = time.perf_counter() - t0
+    value = m * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "circuits/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "n_qubits": w.n, "L": w.L, "layers": w.layers,
+                   "circuits_per_eval": w.n_circuits, "sample_circuits_per_step": m},
+        "cpu_baseline": {"value": value, "unit": "circuits/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{m} evenly strided circuits of {w.name} per step, faithful mode "
+                                   f"(V(theta) re-simulated per circuit, the paper's per-circuit model)"},
+        "e2e": {"value": value, "unit": "circuits/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=1, help="thetas per step (dvqls_cost_dev K)")
+    ap.add_argument("--impl", default="dvqls", choices=["dvqls", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    w = CONFIGS[args.config]()
+
+    if args.impl == "reference":
+        return run_reference(args, w)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2604_14435_b200 import build as pbuild
+    from paper_2604_14435_b200 import dvqls
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if rank == 0 and not os.path.exists(dvqls.LIB_PATH):
+        pbuild.build()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [dvqls.dvqls_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    else:
+        nccl_id = None
+
+    stream = torch.cuda.Stream(device=dev)
+    KT = args.batch
+    chars, co = w.arrays()
+    ctx = dvqls.Context(w.n, w.layers, chars, co, w.bkind, w.b, device=local, rank=rank, world=world,
+                        nccl_id=nccl_id, entangler=w.entangler, stream=stream, timing=True,
+                        max_batch=max(KT, 1))
+    c0, c1 = ctx.local_range()
+    thetas = np.stack([w.theta0(s) for s in range(KT)])
+    th_dev = torch.tensor(thetas, dtype=torch.float64, device=dev)
+    out_dev = torch.empty(5 * KT, dtype=torch.float64, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident timed region ----------------------------------------------------
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.zero_()
+            ctx.cost_dev(KT, th_dev, out_dev)
+        barrier()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        kt = []
+        sampler = ClockSampler(list(range(world))) if rank == 0 else None
+        if sampler:
+            sampler.__enter__()
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record(stream)
+            ctx.cost_dev(KT, th_dev, out_dev)
+            ends[i].record(stream)
+            kt.append(ctx.last_timings())  # events of the library on the same stream
+        barrier()
+        if sampler:
+            sampler.__exit__()
+    dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    dev_ms = max_over_ranks(dev_ms)
+    res = out_dev.view(KT, 5).cpu().numpy()
+    if not np.all(np.isfinite(res[:, 0])):
+        print("error: non-finite cost", res, file=sys.stderr)
+        return 1
+
+    # ---- end-to-end through the host-buffer C ABI ---------------------------------------------
+    e2e_s = 0.0
+    for _ in range(2):
+        ctx.cost_batch(thetas) if KT > 1 else ctx.cost(thetas[0])
+    barrier()
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if KT > 1:
+            ctx.cost_batch(thetas)
+        else:
+            ctx.cost(thetas[0])
+        e2e_s += time.perf_counter() - t0
+    barrier()
+    e2e_s = max_over_ranks(e2e_s)
+
+    # ---- derived numbers -------------------------------------------------------------------------
+    circuits_step = w.n_circuits * KT
+    value = circuits_step * args.steps / (dev_ms * 1e-3)
+    e2e_value = circuits_step * args.steps / e2e_s
+    had_ms = statistics.mean(t["hadamard_ms"] for t in kt)
+    pre_ms = statistics.mean(t["prefix_ms"] for t in kt)
+    red_ms = statistics.mean(t["reduce_ms"] for t in kt)
+    local_c = np.arange(c0, c1)
+    ops = fp64_ops_per_eval(w, local_c) * KT
+    sbytes = smem_bytes_per_eval(w, local_c) * KT
+    peaks, peak_src = load_peaks()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    fmax = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    fp64_peak = 64 * sms * fmax  # FP64 pipe lane-ops/s at max clock
+    smem_peak = 128 * sms * fmax  # B/s at max clock
+    achieved_ops = ops / (had_ms * 1e-3)
+    achieved_smem = sbytes / (had_ms * 1e-3)
+    clocks = sampler.summary() if sampler else None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "circuits/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": dev_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic",
+            "config": {
+                "workload": w.name, "n_qubits": w.n, "L": w.L, "layers": w.layers,
+                "circuits_per_eval": w.n_circuits, "thetas_per_step": KT,
+                "l2": "flushed before every step (256 MiB write, outside the timed events)",
+                "parallelism": f"dp{world} (contiguous circuit blocks, one NCCL allreduce of 4 fp64 per theta)",
+            },
+            "evals_per_s": KT * args.steps / (dev_ms * 1e-3),
+            "kernel_ms": {"prefix": pre_ms, "hadamard": had_ms, "reduce": red_ms},
+            "roofline": {
+                "bound": "alu",
+                "kernel": "hadamard_kernel",
+                "achieved": achieved_ops / 1e12,
+                "peak": fp64_peak / 1e12,
+                "unit": "Top/s",
+                "frac": achieved_ops / fp64_peak,
+                "traffic": traffic_from_profiles(),
+                "note": ("FP64-pipe lane-ops (DADD and DFMA = 1 op each; the kernel is >95% DADD) per launch "
+                         f"= {ops:.4g} (SURVEY §8(d)) / mean CUDA-event time of the kernel on the launching "
+                         f"stream; peak = 64 lanes/clk/SM x {sms} SMs x sm_max_mhz ({peak_src} "
+                         "MEASURED_PEAKS.json)"),
+                "smem": {"achieved": achieved_smem / 1e9, "peak": smem_peak / 1e9, "unit": "GB/s",
+                         "frac": achieved_smem / smem_peak,
+                         "note": "on-chip model bytes: 96N per numerator circuit, 32N per denominator"},
+                "model_frac": max(ops / fp64_peak, sbytes / smem_peak) / (had_ms * 1e-3),
+            },
+            "e2e": {"value": e2e_value, "unit": "circuits/s", "h2d_bytes_per_step": 8 * w.n_params * KT,
+                    "d2h_bytes_per_step": 40 * KT},
+            "gpu_launches": args.steps * ctx.launches_per_call(),
+            "clocks": clocks,
+            "cost": float(res[0, 0]),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(w, thetas[0])
+        print(json.dumps(line), flush=True)
+    ctx.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,156 @@
+/*
+ * dvqls.h - C ABI of libdvqls.so, the B200 (sm_100a) hot path of D-VQLS
+ * (arXiv 2604.14435): per cost call, evaluate all 2(n+1)L^2 Hadamard-test
+ * circuits of the LCU-expanded local VQLS cost, reduce them
+ * coefficient-weighted into (E, Psi), allreduce across ranks and return
+ *     C = 1/2 - 1/2 * Re E / (n * Re Psi).
+ *
+ * Citations are PAPER.md line numbers (P:n) with section / equation /
+ * algorithm, and SURVEY.md sections (§n) for readings of the paper.
+ *
+ *   A = sum_l c_l A_l, A_l Pauli strings            P:372-375 (Eq. 3, §II-B)
+ *   E   = sum_j sum_{l,k} c_l^* c_k <x|A_l U_b Z_j U_b^+ A_k|x>
+ *   Psi =       sum_{l,k} c_l^* c_k <x|A_l A_k|x>    P:380-385 (Eq. 4)
+ *   each expectation = two Hadamard tests (Re, Im)
+ *   x = V(theta)|0>, hardware-efficient ansatz
+ *   local aggregation, Allreduce, C formula         P:389-398, Alg. 1
+ *
+ * Conventions (SURVEY §8(c) readings; listed in DESIGN.md):
+ *   - big-endian: qubit 0 = most significant index bit; Pauli string
+ *     character q acts on qubit q (reading 9);
+ *   - V(theta): `layers` layers; per qubit Ry(t0), Rz(t1), Ry(t2) with
+ *     t_r = theta[(layer*n + q)*3 + r]; then a CNOT ring q -> (q+1) mod n in
+ *     ascending q (none for n = 1), or a CZ ring (readings 6-8);
+ *     Ry(t) = exp(-i t Y/2), Rz(t) = exp(-i t Z/2);
+ *   - P_j = Z_j on system qubit j; U_b applied in the numerator (readings 1-2);
+ *   - Im circuit uses S^dagger after the first ancilla H: <Z_anc> = +Im (reading 10);
+ *   - task t = ((l*L + k)*(n+1) + s), s = 0 denominator, s = 1+j numerator j;
+ *     circuit c = 2t + part, part 0 = Re, 1 = Im (reading 17).
+ *
+ * Threading: a context is not thread-safe; calls on one context must be
+ * serialised by the caller.  All calls return 0 on success or a negative
+ * DVQLS_E_* code; the first error aborts the call and its message is
+ * available from dvqls_last_error().  No CPU fallback exists: without a
+ * usable sm_100 device dvqls_create fails with DVQLS_E_CUDA.
+ */
+#ifndef DVQLS_H
+#define DVQLS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define DVQLS_OK 0
+#define DVQLS_E_ARG (-1)         /* bad size, null pointer, out-of-range option          */
+#define DVQLS_E_PAULI (-2)       /* Pauli character not in {I,X,Y,Z}, or duplicate string */
+#define DVQLS_E_BPREP (-3)       /* | ||b|| - 1 | > 1e-8, or unknown b kind              */
+#define DVQLS_E_DEGENERATE (-4)  /* Re Psi <= 1e-12 (SURVEY §8(c) reading 13)            */
+#define DVQLS_E_CUDA (-5)        /* CUDA runtime error / no sm_100 device                */
+#define DVQLS_E_NCCL (-6)        /* NCCL unavailable or NCCL call failed                 */
+#define DVQLS_E_UNSUPPORTED (-7) /* size this build cannot evaluate                       */
+
+/* ---- b-state preparation U_b ("fixed unitary U_b|0> = |b>") ------ */
+#define DVQLS_B_UNIFORM 0    /* U_b = H^{(x)n}; |b> = uniform superposition          */
+#define DVQLS_B_AMPLITUDES 1 /* U_b = w (I - 2 v v^+ / v^+ v), v = e_0 - conj(w) b,
+                                w = b_0/|b_0| (1 if b_0 = 0); U_b = w I if v = 0
+                                (SURVEY §8(c) reading 5).  C depends on this choice. */
+typedef struct dvqls_bprep {
+  int kind;            /* DVQLS_B_UNIFORM or DVQLS_B_AMPLITUDES                       */
+  const double* amps;  /* AMPLITUDES: 2*2^n doubles, interleaved (re, im), host memory;
+                          copied at create.  Ignored for UNIFORM.                       */
+} dvqls_bprep;
+
+/* ---- options (all fields optional: pass NULL for defaults) ------------- */
+typedef struct dvqls_opts {
+  int device;                  /* CUDA device ordinal; -1 = current device              */
+  int rank;                    /* this process's rank in [0, world)                      */
+  int world;                   /* number of ranks (1 = single GPU)                       */
+  const void* nccl_unique_id;  /* 128-byte ncclUniqueId, identical on all ranks; required
+                                  when world > 1 (see dvqls_nccl_unique_id)              */
+  int entangler;               /* 0 = CNOT ring (default), 1 = CZ ring                   */
+  void* cuda_stream;           /* cudaStream_t for all device work; NULL = library-owned */
+  int timing;                  /* nonzero: record CUDA events around each kernel         */
+  int max_batch;               /* largest K accepted by the *_batch calls (default 16)   */
+} dvqls_opts;
+
+typedef struct dvqls_ctx dvqls_ctx;
+
+/* Build a context: parse the L Pauli strings into
+ * (x_mask, z_mask, n_Y), copy coefficients, build U_b data, allocate device
+ * buffers (the only cudaMalloc calls of the library), pick this rank's
+ * contiguous circuit block [c0, c1) = [rank*C/world, (rank+1)*C/world) of the
+ * C = 2(n+1)L^2 circuits ("strided workload allocation"; a contiguous
+ * block balances equally) and, for world > 1, create the NCCL
+ * communicator.  Collective over all ranks when world > 1.
+ *   n_qubits    system qubits n, 1 <= n <= 10 in this build (else UNSUPPORTED)
+ *   layers      ansatz depth d >= 1; theta has P = 3*n*layers doubles
+ *   n_terms     L >= 1
+ *   pauli_terms L*n characters, row-major (term l at pauli_terms + l*n)
+ *   coeffs      2*L doubles, interleaved (re, im) of c_l
+ * Inputs are copied; the caller may free them on return. */
+int dvqls_create(dvqls_ctx** out, int n_qubits, int layers, int n_terms,
+                 const char* pauli_terms, const double* coeffs,
+                 const dvqls_bprep* b_prep, const dvqls_opts* opts);
+
+/* Free all device and host resources (safe on NULL). */
+void dvqls_destroy(dvqls_ctx* ctx);
+
+/* Term expectations of one theta (host buffers; synchronous).
+ *   theta        P doubles (host)
+ *   out_expvals  2(n+1)L^2 doubles (host), canonical order, index 2t + part;
+ *                every rank receives the full array (allgather over NCCL). */
+int dvqls_terms(dvqls_ctx* ctx, const double* theta, double* out_expvals);
+
+/* Cost of one theta (host buffers; synchronous): the whole hot path
+ * (prefix -> circuits -> weighted reduction -> allreduce -> C).
+ *   out_cost   1 double
+ *   out_E_Psi  NULL or 4 doubles: Re E, Im E, Re Psi, Im Psi (global sums)
+ * Returns DVQLS_E_DEGENERATE (out_cost = NaN) if Re Psi <= 1e-12. */
+int dvqls_cost(dvqls_ctx* ctx, const double* theta, double* out_cost, double* out_E_Psi);
+
+/* K independent thetas in one pass (FD / parameter-shift points), host buffers.
+ *   thetas     K*P doubles, row-major;  1 <= K <= opts.max_batch
+ *   out_costs  K doubles;  out_E_Psi NULL or 4*K doubles
+ * Degenerate entries get NaN and the call returns DVQLS_E_DEGENERATE. */
+int dvqls_cost_batch(dvqls_ctx* ctx, int K, const double* thetas, double* out_costs,
+                     double* out_E_Psi);
+
+/* Device-resident variant: asynchronous on the context stream, no host sync.
+ *   thetas_dev  K*P doubles in device memory
+ *   out_dev     5*K doubles in device memory: per theta (C, Re E, Im E, Re Psi, Im Psi);
+ *               C = NaN when Re Psi <= 1e-12.
+ * Caller synchronises the stream (dvqls_stream) before reading out_dev. */
+int dvqls_cost_dev(dvqls_ctx* ctx, int K, const double* thetas_dev, double* out_dev);
+
+/* Device-resident terms of THIS rank's block [c0, c1) for one theta (async).
+ *   out_dev  (c1 - c0) doubles in device memory */
+int dvqls_terms_local_dev(dvqls_ctx* ctx, const double* theta_dev, double* out_dev);
+
+/* ---- introspection ------------------------------------------------------ */
+const char* dvqls_last_error(const dvqls_ctx* ctx); /* "" if none; static text if ctx NULL */
+int64_t dvqls_num_circuits(const dvqls_ctx* ctx);   /* 2(n+1)L^2 */
+int dvqls_local_range(const dvqls_ctx* ctx, int64_t* c0, int64_t* c1);
+void* dvqls_stream(const dvqls_ctx* ctx);           /* the cudaStream_t in use */
+/* Kernel launches per cost evaluation call (prefix + circuits + reduce [+ finalize]). */
+int dvqls_launches_per_call(const dvqls_ctx* ctx);
+/* With opts.timing: device milliseconds of the last call, measured with CUDA events
+ * on the context stream: ms[0] prefix, ms[1] Hadamard-test kernel, ms[2] reduction
+ * (+ allreduce + finalize), ms[3] whole call.  Returns DVQLS_E_ARG if timing is off. */
+int dvqls_last_timings(const dvqls_ctx* ctx, float* ms4);
+/* Pure host helper (no device access): the contiguous circuit block
+ * [c0, c1) = [floor(C*rank/world), floor(C*(rank+1)/world)) a rank evaluates.
+ * Blocks of consecutive ranks tile [0, C) and differ in size by at most 1. */
+int dvqls_shard_range(int64_t n_circuits, int rank, int world, int64_t* c0, int64_t* c1);
+/* Write a fresh 128-byte ncclUniqueId into out128 (rank 0 calls, then broadcasts). */
+int dvqls_nccl_unique_id(void* out128);
+/* Static build description (arch, supported n range). */
+const char* dvqls_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DVQLS_H */

@@ -1,0 +1,526 @@
+// dvqls_api.cu - the C ABI of libdvqls.so (declared and documented in include/dvqls.h).
+//
+// Host side of the hot path: context build, launch of the
+// sm_100a kernels (kernels.cuh), the cross-rank reduction (a10, "Global
+// Reduction", Alg. 1 Step 4c P:461-463) over a library-owned NCCL communicator,
+// and marshalling of host buffers.  No arithmetic of the method runs here; the
+// host only validates inputs, precomputes the Householder vector of U_b and
+// moves bytes.
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <complex>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/dvqls.h"
+#include "kernels.cuh"
+#include "nccl_dl.h"
+
+using namespace dvqls;
+
+namespace {
+
+constexpr int kMaxQubits = 10;  // SMEM-resident path of this build
+
+struct KernelCfg {
+  const void* fn = nullptr;
+  int warps = 0;
+  size_t smem = 0;
+  int gpw = 0;  // circuit groups per warp
+};
+
+template <int NQ, bool HH, int W>
+KernelCfg make_cfg() {
+  using S = Shape<NQ>;
+  KernelCfg k;
+  k.fn = (const void*)&hadamard_kernel<NQ, W, HH>;
+  k.warps = W;
+  k.gpw = S::GPW;
+  k.smem = sizeof(double2) * (size_t(HH ? 2 : 1) * S::N + size_t(W) * S::GPW * S::N);
+  return k;
+}
+
+// n >= 9 keeps 32 amplitudes per thread: 12 warps (168 registers) or 8 warps
+// (no register cap); DVQLS_WARPS=8 selects the latter (tuning knob).
+template <int NQ, bool HH>
+KernelCfg pick_cfg() {
+  if constexpr (NQ >= 9) {
+    const char* e = getenv("DVQLS_WARPS");
+    if (e && atoi(e) == 8) return make_cfg<NQ, HH, 8>();
+    return make_cfg<NQ, HH, 12>();
+  } else {
+    return make_cfg<NQ, HH, 16>();
+  }
+}
+
+template <bool HH>
+KernelCfg cfg_for(int n) {
+  switch (n) {
+    case 1: return pick_cfg<1, HH>();
+    case 2: return pick_cfg<2, HH>();
+    case 3: return pick_cfg<3, HH>();
+    case 4: return pick_cfg<4, HH>();
+    case 5: return pick_cfg<5, HH>();
+    case 6: return pick_cfg<6, HH>();
+    case 7: return pick_cfg<7, HH>();
+    case 8: return pick_cfg<8, HH>();
+    case 9: return pick_cfg<9, HH>();
+    case 10: return pick_cfg<10, HH>();
+    default: return KernelCfg{};
+  }
+}
+
+}  // namespace
+
+struct dvqls_ctx {
+  int n = 0, layers = 0, L = 0, P = 0, N = 0;
+  int bkind = DVQLS_B_UNIFORM, entangler = 0;
+  int device = 0, rank = 0, world = 1, max_batch = 16, timing = 0;
+  int64_t C = 0, c0 = 0, c1 = 0, chunk = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+
+  KernelCfg kc;
+  int grid = 0;     // CTAs per theta
+  int64_t NG = 0;   // circuit groups per theta
+  int prefix_threads = 0;
+  size_t prefix_smem = 0;
+  double hv_scale = 0.0;
+
+  PauliTerm* d_tab = nullptr;
+  double2* d_coef = nullptr;
+  double2* d_hv = nullptr;
+  double* d_theta = nullptr;     // max_batch * P
+  double2* d_x = nullptr;        // max_batch * N
+  double* d_terms = nullptr;     // max_batch * chunk
+  double* d_partials = nullptr;  // max_batch * NG * 4
+  double* d_ep = nullptr;        // max_batch * 4 (allreduce buffer)
+  double* d_out = nullptr;       // max_batch * 5
+  double* d_gather = nullptr;    // world * chunk (terms allgather)
+  double* h_stage = nullptr;     // pinned staging
+  size_t h_stage_bytes = 0;
+
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool timed_once = false;
+  std::string err;
+};
+
+namespace {
+
+int fail(dvqls_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CK(call)                                                                                 \
+  do {                                                                                           \
+    cudaError_t e_ = (call);                                                                     \
+    if (e_ != cudaSuccess)                                                                       \
+      return fail(ctx, DVQLS_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),     \
+                  __FILE__, __LINE__);                                                           \
+  } while (0)
+
+#define CKN(call)                                                                                \
+  do {                                                                                           \
+    ncclResult_t r_ = (call);                                                                    \
+    if (r_ != ncclSuccess)                                                                       \
+      return fail(ctx, DVQLS_E_NCCL, "%s failed: %s", #call, nccl().GetErrorString(r_));         \
+  } while (0)
+
+thread_local std::string g_create_err;
+
+int launch_eval(dvqls_ctx* ctx, int K, const double* thetas_dev, bool want_cost, double* out_dev) {
+  if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+  prefix_kernel<<<K, ctx->prefix_threads, ctx->prefix_smem, ctx->stream>>>(ctx->n, ctx->layers, ctx->entangler,
+                                                                            thetas_dev, ctx->d_x);
+  CK(cudaGetLastError());
+  if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+  const int64_t Cloc = ctx->c1 - ctx->c0;
+  {
+    dim3 grid(ctx->grid, K);
+    void* args[] = {(void*)&ctx->d_x,   (void*)&ctx->d_tab, (void*)&ctx->d_coef,  (void*)&ctx->d_hv,
+                    (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&ctx->c0, (void*)&Cloc,
+                    (void*)&ctx->d_terms, (void*)&ctx->d_partials};
+    CK(cudaLaunchKernel(ctx->kc.fn, grid, dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
+  }
+  if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+  if (want_cost) {
+    if (ctx->world == 1) {
+      reduce_kernel<<<K, REDUCE_THREADS, 0, ctx->stream>>>(ctx->d_partials, ctx->NG, ctx->n, 1, out_dev);
+      CK(cudaGetLastError());
+    } else {
+      reduce_kernel<<<K, REDUCE_THREADS, 0, ctx->stream>>>(ctx->d_partials, ctx->NG, ctx->n, 0, ctx->d_ep);
+      CK(cudaGetLastError());
+      CKN(nccl().AllReduce(ctx->d_ep, ctx->d_ep, size_t(4) * K, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+      finalize_kernel<<<1, 32 * ((K + 31) / 32), 0, ctx->stream>>>(ctx->d_ep, K, ctx->n, out_dev);
+      CK(cudaGetLastError());
+    }
+  }
+  if (ctx->timing) {
+    CK(cudaEventRecord(ctx->ev[3], ctx->stream));
+    ctx->timed_once = true;
+  }
+  return DVQLS_OK;
+}
+
+void release(dvqls_ctx* c) {
+  if (!c) return;
+  if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+  cudaFree(c->d_tab); cudaFree(c->d_coef); cudaFree(c->d_hv); cudaFree(c->d_theta); cudaFree(c->d_x);
+  cudaFree(c->d_terms); cudaFree(c->d_partials); cudaFree(c->d_ep); cudaFree(c->d_out); cudaFree(c->d_gather);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  for (auto& e : c->ev) if (e) cudaEventDestroy(e);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, const double* coeffs,
+                 const dvqls_bprep* bprep, const dvqls_opts* opts) {
+  g_create_err.clear();
+  dvqls_ctx* ctx = nullptr;
+  auto early = [&](int code, const char* msg) {
+    g_create_err = msg;
+    return code;
+  };
+  if (!out) return early(DVQLS_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || n > 24) return early(DVQLS_E_ARG, "n_qubits must be in [1, 24]");
+  if (layers < 1) return early(DVQLS_E_ARG, "layers must be >= 1");
+  if (L < 1) return early(DVQLS_E_ARG, "n_terms must be >= 1");
+  if (!paulis || !coeffs) return early(DVQLS_E_ARG, "pauli_terms / coeffs is NULL");
+  if (n > kMaxQubits) return early(DVQLS_E_UNSUPPORTED, "this build evaluates n <= 10 (SMEM-resident path)");
+
+  ctx = new dvqls_ctx();
+  ctx->n = n; ctx->layers = layers; ctx->L = L; ctx->P = 3 * n * layers; ctx->N = 1 << n;
+  if (opts) {
+    ctx->device = opts->device; ctx->rank = opts->rank; ctx->world = opts->world;
+    ctx->entangler = opts->entangler; ctx->timing = opts->timing;
+    if (opts->max_batch > 0) ctx->max_batch = opts->max_batch;
+  } else {
+    ctx->device = -1; ctx->rank = 0; ctx->world = 1;
+  }
+  auto bail = [&](int code) {
+    g_create_err = ctx->err;
+    release(ctx);
+    delete ctx;
+    return code;
+  };
+  if (ctx->world < 1 || ctx->rank < 0 || ctx->rank >= ctx->world) {
+    fail(ctx, DVQLS_E_ARG, "rank/world out of range");
+    return bail(DVQLS_E_ARG);
+  }
+  if (ctx->entangler != 0 && ctx->entangler != 1) {
+    fail(ctx, DVQLS_E_ARG, "entangler must be 0 (CNOT ring) or 1 (CZ ring)");
+    return bail(DVQLS_E_ARG);
+  }
+  if (ctx->world > 1 && !(opts && opts->nccl_unique_id)) {
+    fail(ctx, DVQLS_E_ARG, "world > 1 requires opts.nccl_unique_id");
+    return bail(DVQLS_E_ARG);
+  }
+
+  // ---- a1: Pauli strings -> (x_mask, z_mask, n_Y), big-endian (reading 9) ----
+  std::vector<PauliTerm> tab(L);
+  std::set<std::string> seen;
+  for (int l = 0; l < L; ++l) {
+    std::string s(paulis + size_t(l) * n, size_t(n));
+    if (!seen.insert(s).second) {
+      fail(ctx, DVQLS_E_PAULI, "duplicate Pauli string %s (term %d)", s.c_str(), l);
+      return bail(DVQLS_E_PAULI);
+    }
+    PauliTerm t{0, 0, 0, 0};
+    for (int q = 0; q < n; ++q) {
+      const uint32_t bit = 1u << (n - 1 - q);
+      switch (s[q]) {
+        case 'I': break;
+        case 'X': t.xm |= bit; break;
+        case 'Y': t.xm |= bit; t.zm |= bit; t.ny += 1; break;
+        case 'Z': t.zm |= bit; break;
+        default:
+          fail(ctx, DVQLS_E_PAULI, "bad Pauli character 0x%02x in term %d", (unsigned char)s[q], l);
+          return bail(DVQLS_E_PAULI);
+      }
+    }
+    tab[l] = t;
+  }
+  std::vector<double2> coef(L);
+  for (int l = 0; l < L; ++l) coef[l] = make_double2(coeffs[2 * l], coeffs[2 * l + 1]);
+
+  // ---- U_b: uniform (H^{(x)n}) or Householder vector (reading 5) -------------
+  std::vector<double2> hv;
+  if (bprep) ctx->bkind = bprep->kind;
+  if (ctx->bkind == DVQLS_B_AMPLITUDES) {
+    if (!bprep->amps) {
+      fail(ctx, DVQLS_E_BPREP, "AMPLITUDES b_prep needs amps");
+      return bail(DVQLS_E_BPREP);
+    }
+    const int N = ctx->N;
+    std::vector<std::complex<double>> b(N);
+    double nn = 0;
+    for (int i = 0; i < N; ++i) {
+      b[i] = {bprep->amps[2 * i], bprep->amps[2 * i + 1]};
+      nn += std::norm(b[i]);
+    }
+    if (std::fabs(std::sqrt(nn) - 1.0) > 1e-8) {
+      fail(ctx, DVQLS_E_BPREP, "| ||b|| - 1 | = %.3e > 1e-8", std::fabs(std::sqrt(nn) - 1.0));
+      return bail(DVQLS_E_BPREP);
+    }
+    const std::complex<double> w = std::abs(b[0]) > 0 ? b[0] / std::abs(b[0]) : std::complex<double>(1, 0);
+    hv.resize(N);
+    double vv = 0;
+    for (int i = 0; i < N; ++i) {
+      std::complex<double> v = (i == 0 ? 1.0 : 0.0) - std::conj(w) * b[i];
+      hv[i] = make_double2(v.real(), v.imag());
+      vv += std::norm(v);
+    }
+    ctx->hv_scale = vv > 0 ? 2.0 / vv : 0.0;
+  } else if (ctx->bkind != DVQLS_B_UNIFORM) {
+    fail(ctx, DVQLS_E_BPREP, "unknown b_prep kind %d", ctx->bkind);
+    return bail(DVQLS_E_BPREP);
+  }
+
+  // ---- device, stream, kernel configuration ---------------------------------
+  if ((ctx->device >= 0 && cudaSetDevice(ctx->device) != cudaSuccess) ||
+      cudaGetDevice(&ctx->device) != cudaSuccess) {
+    fail(ctx, DVQLS_E_CUDA, "no CUDA device");
+    return bail(DVQLS_E_CUDA);
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, ctx->device) != cudaSuccess || prop.major != 10) {
+    fail(ctx, DVQLS_E_CUDA, "libdvqls is built for sm_100a only (device cc %d.%d)", prop.major, prop.minor);
+    return bail(DVQLS_E_CUDA);
+  }
+  if (opts && opts->cuda_stream) {
+    ctx->stream = (cudaStream_t)opts->cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      fail(ctx, DVQLS_E_CUDA, "cudaStreamCreate failed");
+      return bail(DVQLS_E_CUDA);
+    }
+    ctx->own_stream = true;
+  }
+  ctx->kc = ctx->bkind == DVQLS_B_AMPLITUDES ? cfg_for<true>(n) : cfg_for<false>(n);
+  if (cudaFuncSetAttribute(ctx->kc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->kc.smem)) !=
+      cudaSuccess) {
+    fail(ctx, DVQLS_E_CUDA, "cannot reserve %zu B of shared memory", ctx->kc.smem);
+    return bail(DVQLS_E_CUDA);
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ctx->kc.fn, ctx->kc.warps * 32, ctx->kc.smem);
+  if (occ < 1) {
+    fail(ctx, DVQLS_E_CUDA, "hadamard kernel cannot be resident (smem %zu B)", ctx->kc.smem);
+    return bail(DVQLS_E_CUDA);
+  }
+
+  ctx->C = 2 * int64_t(n + 1) * L * L;
+  dvqls_shard_range(ctx->C, ctx->rank, ctx->world, &ctx->c0, &ctx->c1);
+  ctx->chunk = (ctx->C + ctx->world - 1) / ctx->world;
+  const int64_t Cloc = ctx->c1 - ctx->c0;
+  const int64_t groups_per_cta = int64_t(ctx->kc.warps) * ctx->kc.gpw;
+  int64_t want = int64_t(prop.multiProcessorCount) * occ;
+  const int64_t need = (Cloc + groups_per_cta - 1) / groups_per_cta;
+  ctx->grid = int(std::max<int64_t>(1, std::min(want, need)));
+  ctx->NG = int64_t(ctx->grid) * groups_per_cta;
+
+  ctx->prefix_threads = std::min(512, std::max(32, ctx->N / 2));
+  ctx->prefix_smem = sizeof(double2) * (2 * size_t(ctx->N) + 4 * size_t(n) * layers);
+  if (cudaFuncSetAttribute((const void*)&prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(ctx->prefix_smem)) != cudaSuccess) {
+    fail(ctx, DVQLS_E_CUDA, "prefix kernel smem %zu B", ctx->prefix_smem);
+    return bail(DVQLS_E_CUDA);
+  }
+
+  // ---- device buffers (the library's only allocations) -----------------------
+  const int KB = ctx->max_batch;
+  auto alloc = [&](void** p, size_t bytes) { return cudaMalloc(p, bytes > 0 ? bytes : 16); };
+  if (alloc((void**)&ctx->d_tab, sizeof(PauliTerm) * L) || alloc((void**)&ctx->d_coef, sizeof(double2) * L) ||
+      alloc((void**)&ctx->d_hv, sizeof(double2) * ctx->N) ||
+      alloc((void**)&ctx->d_theta, sizeof(double) * KB * ctx->P) ||
+      alloc((void**)&ctx->d_x, sizeof(double2) * KB * ctx->N) ||
+      alloc((void**)&ctx->d_terms, sizeof(double) * KB * ctx->chunk) ||
+      alloc((void**)&ctx->d_partials, sizeof(double) * KB * ctx->NG * 4) ||
+      alloc((void**)&ctx->d_ep, sizeof(double) * KB * 4) || alloc((void**)&ctx->d_out, sizeof(double) * KB * 5) ||
+      (ctx->world > 1 && alloc((void**)&ctx->d_gather, sizeof(double) * ctx->world * ctx->chunk))) {
+    fail(ctx, DVQLS_E_CUDA, "cudaMalloc failed");
+    return bail(DVQLS_E_CUDA);
+  }
+  ctx->h_stage_bytes = sizeof(double) * std::max<size_t>(size_t(KB) * (ctx->P + 5), 64);
+  if (cudaMallocHost((void**)&ctx->h_stage, ctx->h_stage_bytes) != cudaSuccess) {
+    fail(ctx, DVQLS_E_CUDA, "cudaMallocHost failed");
+    return bail(DVQLS_E_CUDA);
+  }
+  if (cudaMemcpy(ctx->d_tab, tab.data(), sizeof(PauliTerm) * L, cudaMemcpyHostToDevice) ||
+      cudaMemcpy(ctx->d_coef, coef.data(), sizeof(double2) * L, cudaMemcpyHostToDevice) ||
+      (!hv.empty() && cudaMemcpy(ctx->d_hv, hv.data(), sizeof(double2) * ctx->N, cudaMemcpyHostToDevice))) {
+    fail(ctx, DVQLS_E_CUDA, "table upload failed");
+    return bail(DVQLS_E_CUDA);
+  }
+  if (ctx->timing)
+    for (auto& e : ctx->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) {
+        fail(ctx, DVQLS_E_CUDA, "cudaEventCreate failed");
+        return bail(DVQLS_E_CUDA);
+      }
+
+  // ---- NCCL communicator (a10) -------------------------------------------------
+  if (ctx->world > 1) {
+    if (!nccl().ok) {
+      fail(ctx, DVQLS_E_NCCL, "libnccl.so.2 not loadable");
+      return bail(DVQLS_E_NCCL);
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, opts->nccl_unique_id, sizeof id);
+    ncclResult_t r = nccl().CommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
+    if (r != ncclSuccess) {
+      fail(ctx, DVQLS_E_NCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
+      ctx->comm = nullptr;
+      return bail(DVQLS_E_NCCL);
+    }
+  }
+  *out = ctx;
+  return DVQLS_OK;
+}
+
+void dvqls_destroy(dvqls_ctx* ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->stream);
+  release(ctx);
+  delete ctx;
+}
+
+int dvqls_cost_dev(dvqls_ctx* ctx, int K, const double* thetas_dev, double* out_dev) {
+  if (!ctx) return DVQLS_E_ARG;
+  ctx->err.clear();
+  if (K < 1 || K > ctx->max_batch) return fail(ctx, DVQLS_E_ARG, "K=%d outside [1, max_batch=%d]", K, ctx->max_batch);
+  if (!thetas_dev || !out_dev) return fail(ctx, DVQLS_E_ARG, "NULL device pointer");
+  return launch_eval(ctx, K, thetas_dev, true, out_dev);
+}
+
+int dvqls_terms_local_dev(dvqls_ctx* ctx, const double* theta_dev, double* out_dev) {
+  if (!ctx) return DVQLS_E_ARG;
+  ctx->err.clear();
+  if (!theta_dev || !out_dev) return fail(ctx, DVQLS_E_ARG, "NULL device pointer");
+  int rc = launch_eval(ctx, 1, theta_dev, false, nullptr);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(out_dev, ctx->d_terms, sizeof(double) * (ctx->c1 - ctx->c0), cudaMemcpyDeviceToDevice,
+                     ctx->stream));
+  return DVQLS_OK;
+}
+
+int dvqls_cost_batch(dvqls_ctx* ctx, int K, const double* thetas, double* out_costs, double* out_E_Psi) {
+  if (!ctx) return DVQLS_E_ARG;
+  ctx->err.clear();
+  if (K < 1 || K > ctx->max_batch) return fail(ctx, DVQLS_E_ARG, "K=%d outside [1, max_batch=%d]", K, ctx->max_batch);
+  if (!thetas || !out_costs) return fail(ctx, DVQLS_E_ARG, "NULL host pointer");
+  const size_t tb = sizeof(double) * size_t(K) * ctx->P;
+  std::memcpy(ctx->h_stage, thetas, tb);
+  CK(cudaMemcpyAsync(ctx->d_theta, ctx->h_stage, tb, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = launch_eval(ctx, K, ctx->d_theta, true, ctx->d_out);
+  if (rc) return rc;
+  double* h_out = ctx->h_stage + size_t(K) * ctx->P;
+  CK(cudaMemcpyAsync(h_out, ctx->d_out, sizeof(double) * 5 * K, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  bool degenerate = false;
+  for (int k = 0; k < K; ++k) {
+    out_costs[k] = h_out[5 * k];
+    if (out_E_Psi)
+      for (int j = 0; j < 4; ++j) out_E_Psi[4 * k + j] = h_out[5 * k + 1 + j];
+    if (!(h_out[5 * k + 3] > 1e-12)) degenerate = true;
+  }
+  if (degenerate) return fail(ctx, DVQLS_E_DEGENERATE, "Re Psi <= 1e-12 (singular A on the ansatz state)");
+  return DVQLS_OK;
+}
+
+int dvqls_cost(dvqls_ctx* ctx, const double* theta, double* out_cost, double* out_E_Psi) {
+  return dvqls_cost_batch(ctx, 1, theta, out_cost, out_E_Psi);
+}
+
+int dvqls_terms(dvqls_ctx* ctx, const double* theta, double* out) {
+  if (!ctx) return DVQLS_E_ARG;
+  ctx->err.clear();
+  if (!theta || !out) return fail(ctx, DVQLS_E_ARG, "NULL host pointer");
+  std::memcpy(ctx->h_stage, theta, sizeof(double) * ctx->P);
+  CK(cudaMemcpyAsync(ctx->d_theta, ctx->h_stage, sizeof(double) * ctx->P, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = launch_eval(ctx, 1, ctx->d_theta, false, nullptr);
+  if (rc) return rc;
+  if (ctx->world == 1) {
+    CK(cudaMemcpyAsync(out, ctx->d_terms, sizeof(double) * ctx->C, cudaMemcpyDeviceToHost, ctx->stream));
+  } else {
+    CKN(nccl().AllGather(ctx->d_terms, ctx->d_gather, size_t(ctx->chunk), ncclDouble, ctx->comm, ctx->stream));
+    for (int r = 0; r < ctx->world; ++r) {
+      const int64_t a = ctx->C * r / ctx->world, b = ctx->C * (r + 1) / ctx->world;
+      CK(cudaMemcpyAsync(out + a, ctx->d_gather + size_t(r) * ctx->chunk, sizeof(double) * (b - a),
+                         cudaMemcpyDeviceToHost, ctx->stream));
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DVQLS_OK;
+}
+
+const char* dvqls_last_error(const dvqls_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_err.c_str();
+}
+
+int64_t dvqls_num_circuits(const dvqls_ctx* ctx) { return ctx ? ctx->C : -1; }
+
+int dvqls_local_range(const dvqls_ctx* ctx, int64_t* c0, int64_t* c1) {
+  if (!ctx || !c0 || !c1) return DVQLS_E_ARG;
+  *c0 = ctx->c0;
+  *c1 = ctx->c1;
+  return DVQLS_OK;
+}
+
+void* dvqls_stream(const dvqls_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int dvqls_launches_per_call(const dvqls_ctx* ctx) {
+  if (!ctx) return DVQLS_E_ARG;
+  return ctx->world == 1 ? 3 : 4;  // prefix, hadamard, reduce [, finalize]  (+ NCCL kernel)
+}
+
+int dvqls_last_timings(const dvqls_ctx* c, float* ms) {
+  dvqls_ctx* ctx = const_cast<dvqls_ctx*>(c);
+  if (!ctx || !ms || !ctx->timing || !ctx->timed_once) return DVQLS_E_ARG;
+  CK(cudaEventSynchronize(ctx->ev[3]));
+  CK(cudaEventElapsedTime(&ms[0], ctx->ev[0], ctx->ev[1]));
+  CK(cudaEventElapsedTime(&ms[1], ctx->ev[1], ctx->ev[2]));
+  CK(cudaEventElapsedTime(&ms[2], ctx->ev[2], ctx->ev[3]));
+  CK(cudaEventElapsedTime(&ms[3], ctx->ev[0], ctx->ev[3]));
+  return DVQLS_OK;
+}
+
+int dvqls_nccl_unique_id(void* out128) {
+  if (!out128) return DVQLS_E_ARG;
+  if (!nccl().ok) return DVQLS_E_NCCL;
+  ncclUniqueId id;
+  if (nccl().GetUniqueId(&id) != ncclSuccess) return DVQLS_E_NCCL;
+  std::memcpy(out128, &id, sizeof id);
+  return DVQLS_OK;
+}
+
+int dvqls_shard_range(int64_t n_circuits, int rank, int world, int64_t* c0, int64_t* c1) {
+  if (n_circuits < 0 || world < 1 || rank < 0 || rank >= world || !c0 || !c1) return DVQLS_E_ARG;
+  *c0 = n_circuits * rank / world;
+  *c1 = n_circuits * (rank + 1) / world;
+  return DVQLS_OK;
+}
+
+const char* dvqls_build_info(void) {
+  return "libdvqls sm_100a; SMEM-resident Hadamard-test path n=1..10; fp64 (complex128); NCCL via dlopen";
+}
+
+}  // extern "C"

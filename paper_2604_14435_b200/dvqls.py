@@ -1,0 +1,262 @@
+"""Thin ctypes binding of libdvqls.so (include/dvqls.h), same names as the C ABI.
+
+Argument marshalling only: every step of the hot path runs in the library's
+sm_100a kernels.  There is no CPU fallback; if the in-tree ``libdvqls.so`` is
+missing or the device is not an sm_100 part the calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdvqls.so")
+
+DVQLS_OK = 0
+DVQLS_E_ARG = -1
+DVQLS_E_PAULI = -2
+DVQLS_E_BPREP = -3
+DVQLS_E_DEGENERATE = -4
+DVQLS_E_CUDA = -5
+DVQLS_E_NCCL = -6
+DVQLS_E_UNSUPPORTED = -7
+DVQLS_B_UNIFORM = 0
+DVQLS_B_AMPLITUDES = 1
+
+EXPORTED = [
+    "dvqls_create", "dvqls_destroy", "dvqls_terms", "dvqls_cost", "dvqls_cost_batch",
+    "dvqls_cost_dev", "dvqls_terms_local_dev", "dvqls_last_error", "dvqls_num_circuits",
+    "dvqls_local_range", "dvqls_stream", "dvqls_launches_per_call", "dvqls_last_timings",
+    "dvqls_nccl_unique_id", "dvqls_build_info", "dvqls_shard_range",
+]
+
+
+class DvqlsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"dvqls error {code}: {msg}")
+        self.code = code
+
+
+class DegenerateError(DvqlsError):
+    pass
+
+
+class _BPrep(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("amps", ctypes.POINTER(ctypes.c_double))]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
+                ("nccl_unique_id", ctypes.c_void_p), ("entangler", ctypes.c_int),
+                ("cuda_stream", ctypes.c_void_p), ("timing", ctypes.c_int), ("max_batch", ctypes.c_int)]
+
+
+_lib = None
+
+
+def load():
+    """Load the in-tree libdvqls.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"CUDA extension missing: {LIB_PATH} (run python -m paper_2604_14435_b200.build)")
+    L = ctypes.CDLL(LIB_PATH)
+    dp = ctypes.POINTER(ctypes.c_double)
+    vp = ctypes.c_void_p
+    L.dvqls_create.argtypes = [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                               dp, ctypes.POINTER(_BPrep), ctypes.POINTER(_Opts)]
+    L.dvqls_destroy.argtypes = [vp]
+    L.dvqls_destroy.restype = None
+    L.dvqls_terms.argtypes = [vp, dp, dp]
+    L.dvqls_cost.argtypes = [vp, dp, dp, dp]
+    L.dvqls_cost_batch.argtypes = [vp, ctypes.c_int, dp, dp, dp]
+    L.dvqls_cost_dev.argtypes = [vp, ctypes.c_int, vp, vp]
+    L.dvqls_terms_local_dev.argtypes = [vp, vp, vp]
+    L.dvqls_last_error.argtypes = [vp]
+    L.dvqls_last_error.restype = ctypes.c_char_p
+    L.dvqls_num_circuits.argtypes = [vp]
+    L.dvqls_num_circuits.restype = ctypes.c_int64
+    L.dvqls_local_range.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+    L.dvqls_stream.argtypes = [vp]
+    L.dvqls_stream.restype = vp
+    L.dvqls_launches_per_call.argtypes = [vp]
+    L.dvqls_last_timings.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
+    L.dvqls_nccl_unique_id.argtypes = [vp]
+    L.dvqls_build_info.restype = ctypes.c_char_p
+    L.dvqls_shard_range.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
+                                    ctypes.POINTER(ctypes.c_int64)]
+    for name in EXPORTED:
+        if name not in ("dvqls_destroy", "dvqls_last_error", "dvqls_num_circuits", "dvqls_stream",
+                        "dvqls_build_info"):
+            getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _dp(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _ptr(x):
+    return ctypes.c_void_p(x.data_ptr() if hasattr(x, "data_ptr") else int(x))
+
+
+def _check(rc, ctx=None):
+    if rc == DVQLS_OK:
+        return
+    msg = load().dvqls_last_error(ctx).decode()
+    if rc == DVQLS_E_DEGENERATE:
+        raise DegenerateError(rc, msg)
+    raise DvqlsError(rc, msg)
+
+
+def dvqls_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().dvqls_nccl_unique_id(buf))
+    return buf.raw
+
+
+def dvqls_shard_range(n_circuits: int, rank: int, world: int):
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().dvqls_shard_range(int(n_circuits), int(rank), int(world), ctypes.byref(a), ctypes.byref(b)))
+    return int(a.value), int(b.value)
+
+
+def dvqls_build_info() -> str:
+    return load().dvqls_build_info().decode()
+
+
+class Context:
+    """Owns one dvqls_ctx*.  Methods mirror the C entry points."""
+
+    def __init__(self, n, layers, paulis: bytes, coeffs, bkind=DVQLS_B_UNIFORM, b=None, device=-1, rank=0,
+                 world=1, nccl_id: bytes | None = None, entangler=0, stream=None, timing=False, max_batch=16):
+        L = load()
+        self.n, self.layers = int(n), int(layers)
+        self.P = 3 * self.n * self.layers
+        self.L = len(paulis) // self.n
+        if len(paulis) != self.L * self.n:
+            raise ValueError("pauli_terms length must be n_terms * n")
+        co = np.ascontiguousarray(coeffs, dtype=np.float64)
+        if co.dtype != np.float64 or co.size != 2 * self.L:
+            raise ValueError("coeffs must be 2*L interleaved doubles")
+        self._keep = []
+        bp = _BPrep(bkind, None)
+        if bkind == DVQLS_B_AMPLITUDES:
+            amps = np.ascontiguousarray(np.asarray(b, dtype=np.complex128)).view(np.float64).copy()
+            self._keep.append(amps)
+            bp.amps = _dp(amps)
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            self._keep.append(idbuf)
+        sp = None
+        if stream is not None:
+            sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        op = _Opts(device, rank, world, ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None,
+                   entangler, sp, 1 if timing else 0, max_batch)
+        h = ctypes.c_void_p()
+        rc = L.dvqls_create(ctypes.byref(h), self.n, self.layers, self.L, paulis, _dp(co), ctypes.byref(bp),
+                            ctypes.byref(op))
+        _check(rc, None)
+        self.h = h
+        self.max_batch = max_batch
+
+    # --- host-buffer entry points --------------------------------------------
+    def terms(self, theta) -> np.ndarray:
+        th = self._theta(theta, 1)
+        out = np.empty(self.num_circuits(), dtype=np.float64)
+        _check(load().dvqls_terms(self.h, _dp(th), _dp(out)), self.h)
+        return out
+
+    def cost(self, theta, with_E_Psi=False):
+        th = self._theta(theta, 1)
+        c = np.empty(1)
+        ep = np.empty(4)
+        _check(load().dvqls_cost(self.h, _dp(th), _dp(c), _dp(ep)), self.h)
+        return (float(c[0]), complex(ep[0], ep[1]), complex(ep[2], ep[3])) if with_E_Psi else float(c[0])
+
+    def cost_batch(self, thetas):
+        th = np.ascontiguousarray(thetas, dtype=np.float64)
+        K = th.shape[0]
+        th = self._theta(th, K)
+        c = np.empty(K)
+        ep = np.empty(4 * K)
+        _check(load().dvqls_cost_batch(self.h, K, _dp(th), _dp(c), _dp(ep)), self.h)
+        return c, ep.reshape(K, 4)
+
+    # --- device-resident entry points (torch tensors or raw pointers) --------
+    def cost_dev(self, K, thetas_dev, out_dev):
+        _check(load().dvqls_cost_dev(self.h, int(K), _ptr(thetas_dev), _ptr(out_dev)), self.h)
+
+    def terms_local_dev(self, theta_dev, out_dev):
+        _check(load().dvqls_terms_local_dev(self.h, _ptr(theta_dev), _ptr(out_dev)), self.h)
+
+    # --- introspection -----------------------------------------------------------
+    def num_circuits(self) -> int:
+        return int(load().dvqls_num_circuits(self.h))
+
+    def local_range(self):
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _check(load().dvqls_local_range(self.h, ctypes.byref(a), ctypes.byref(b)), self.h)
+        return int(a.value), int(b.value)
+
+    def stream_ptr(self) -> int:
+        return int(load().dvqls_stream(self.h) or 0)
+
+    def launches_per_call(self) -> int:
+        return int(load().dvqls_launches_per_call(self.h))
+
+    def last_timings(self):
+        ms = (ctypes.c_float * 4)()
+        _check(load().dvqls_last_timings(self.h, ms), self.h)
+        return {"prefix_ms": ms[0], "hadamard_ms": ms[1], "reduce_ms": ms[2], "call_ms": ms[3]}
+
+    def destroy(self):
+        if getattr(self, "h", None):
+            load().dvqls_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    def _theta(self, theta, K):
+        th = np.ascontiguousarray(theta, dtype=np.float64).reshape(-1)
+        if th.size != K * self.P:
+            raise ValueError(f"theta must have K*P = {K}*{self.P} entries (P = 3 n d)")
+        return th
+
+
+# C-ABI-named functional wrappers --------------------------------------------------
+def dvqls_create(n_qubits, layers, pauli_terms: bytes, coeffs, b_prep=(DVQLS_B_UNIFORM, None), **opts) -> Context:
+    kind, amps = b_prep
+    return Context(n_qubits, layers, pauli_terms, coeffs, kind, amps, **opts)
+
+
+def dvqls_terms(ctx: Context, theta) -> np.ndarray:
+    return ctx.terms(theta)
+
+
+def dvqls_cost(ctx: Context, theta) -> float:
+    return ctx.cost(theta)
+
+
+def dvqls_cost_batch(ctx: Context, thetas):
+    return ctx.cost_batch(thetas)[0]
+
+
+def dvqls_destroy(ctx: Context) -> None:
+    ctx.destroy()
+
+
+def from_workload(w, **opts) -> Context:
+    """Context for a dvqls_inputs.configs.Workload."""
+    chars, co = w.arrays()
+    return Context(w.n, w.layers, chars, co, w.bkind, w.b, entangler=w.entangler, **opts)

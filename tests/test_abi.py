@@ -1,0 +1,104 @@
+"""C-ABI boundary checks that need no GPU: the in-tree libdvqls.so builds, loads,
+exports every symbol include/dvqls.h declares, and rejects bad arguments with
+the documented status codes before touching a device."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+import paper_2604_14435_b200 as pkg
+from paper_2604_14435_b200 import build as pbuild
+from paper_2604_14435_b200 import dvqls
+
+
+@pytest.fixture(scope="module")
+def lib():
+    pbuild.build()
+    return dvqls.load()
+
+
+def _declared():
+    h = open(os.path.join(ROOT, "include", "dvqls.h")).read()
+    h = re.sub(r"/\*.*?\*/", "", h, flags=re.S)
+    return sorted(set(re.findall(r"\b(dvqls_[a-z_0-9]+)\s*\(", h)))
+
+
+def test_exports_every_declared_symbol(lib):
+    names = _declared()
+    assert "dvqls_create" in names and "dvqls_cost" in names and "dvqls_terms" in names
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(dvqls.EXPORTED)
+
+
+def test_built_for_sm100a_only():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", dvqls.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(80|86|89|90)\b", out)
+
+
+def _create(lib, n=2, layers=1, paulis=b"IXZY", coeffs=None, bprep=None):
+    L = max(1, len(paulis) // max(n, 1))
+    co = np.ones(2 * L) if coeffs is None else coeffs
+    h = ctypes.c_void_p()
+    rc = lib.dvqls_create(ctypes.byref(h), n, layers, L, paulis,
+                          co.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), bprep, None)
+    return rc, lib.dvqls_last_error(None).decode()
+
+
+def test_argument_errors_without_device(lib):
+    assert _create(lib, n=0)[0] == dvqls.DVQLS_E_ARG
+    assert _create(lib, n=25, paulis=b"I" * 25)[0] == dvqls.DVQLS_E_ARG
+    assert _create(lib, layers=0)[0] == dvqls.DVQLS_E_ARG
+    rc, msg = _create(lib, n=11, paulis=b"I" * 11)
+    assert rc == dvqls.DVQLS_E_UNSUPPORTED and "n <= 10" in msg
+    rc, msg = _create(lib, paulis=b"IXQY")
+    assert rc == dvqls.DVQLS_E_PAULI and "bad Pauli" in msg
+    rc, msg = _create(lib, paulis=b"IXIX")
+    assert rc == dvqls.DVQLS_E_PAULI and "duplicate" in msg
+    bp = dvqls._BPrep(1, None)
+    assert _create(lib, bprep=ctypes.byref(bp))[0] == dvqls.DVQLS_E_BPREP
+    amps = np.array([1.0, 0, 1.0, 0, 0, 0, 0, 0])  # ||b|| = sqrt2
+    bp = dvqls._BPrep(1, amps.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    rc, msg = _create(lib, bprep=ctypes.byref(bp))
+    assert rc == dvqls.DVQLS_E_BPREP and "1e-8" in msg
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_no_gpu_fails_loudly(lib):
+    rc, msg = _create(lib)
+    assert rc == dvqls.DVQLS_E_CUDA
+    with pytest.raises(dvqls.DvqlsError):
+        dvqls.Context(2, 1, b"IXZY", np.ones(4))
+
+
+def test_shard_ranges_tile_the_circuits(lib):
+    for C in (0, 1, 7, 2560, 90112, 360448):
+        for W in (1, 2, 3, 4, 8):
+            prev = 0
+            sizes = []
+            for r in range(W):
+                a, b = dvqls.dvqls_shard_range(C, r, W)
+                assert a == prev
+                prev = b
+                sizes.append(b - a)
+            assert prev == C and max(sizes) - min(sizes) <= 1
+    with pytest.raises(dvqls.DvqlsError):
+        dvqls.dvqls_shard_range(10, 2, 2)
+
+
+def test_product_package_does_not_import_oracle():
+    """The product path must not route through the oracle (or any CPU path)."""
+    for dirpath, _, files in os.walk(os.path.dirname(pkg.__file__)):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle\b", src, re.M), f
+                assert "oracle/" not in src and "liboracle" not in src, f

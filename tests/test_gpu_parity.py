@@ -1,0 +1,158 @@
+"""GPU parity: libdvqls.so (through the C ABI) vs the CPU oracle, element by element.
+
+Tolerance (BASELINE.json north_star): 1e-10 absolute per term expectation and
+on the cost, fp64.  Inputs are the seeded workloads of dvqls_inputs; every
+expected value comes from oracle/ (gate-by-gate simulator + plain aggregation).
+"""
+
+import numpy as np
+import pytest
+
+from dvqls_inputs import configs
+from oracle import cost as ocost
+from oracle import sim
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def dv():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_14435_b200 import build, dvqls
+    build.build()
+    dvqls.load()
+    return dvqls
+
+
+def _check_workload(dv, w, theta=None, idx=None, check_cost=True):
+    th = w.theta0() if theta is None else theta
+    ctx = dv.from_workload(w)
+    try:
+        g = ctx.terms(th)
+        ref = sim.workload_terms(w, th, idx=idx)
+        got = g if idx is None else g[idx]
+        err = np.max(np.abs(got - ref))
+        assert err <= TOL, f"{w.name}: max |term err| = {err:.3e}"
+        if check_cost:
+            C, E, Psi = ctx.cost(th, with_E_Psi=True)
+            if idx is None:
+                Cr, Er, Pr = ocost.cost(ref, ocost.coeffs_of(w), w.n, w.L)
+            else:  # reduction check at full size: oracle aggregation of the GPU terms
+                Cr, Er, Pr = ocost.cost(g, ocost.coeffs_of(w), w.n, w.L)
+            assert abs(C - Cr) <= TOL, (C, Cr)
+            assert abs(E - Er) <= TOL * max(1, abs(Er)) and abs(Psi - Pr) <= TOL * max(1, abs(Pr))
+        return g
+    finally:
+        ctx.destroy()
+
+
+def test_cfg1_tridiag_n4(dv):
+    _check_workload(dv, configs.cfg1())
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_cfg2_hele_shaw(dv, seed):
+    _check_workload(dv, configs.cfg2_velocity(seed))
+    _check_workload(dv, configs.cfg2_pressure(seed))  # Householder U_b path
+
+
+@pytest.mark.parametrize("n", list(range(1, 11)))
+@pytest.mark.parametrize("amp", [False, True])
+def test_random_lcu_every_n(dv, n, amp):
+    """Non-Hermitian random LCUs (Im path), uniform and Householder U_b, n = 1..10."""
+    L = min(5, 4 ** n)
+    w = configs.random_workload(n, L, 2, seed=100 + n, amplitudes=amp)
+    _check_workload(dv, w)
+
+
+@pytest.mark.parametrize("n", [2, 4, 7])
+def test_cz_ring_entangler(dv, n):
+    w = configs.random_workload(n, 4, 3, seed=7 * n, entangler=1)
+    _check_workload(dv, w)
+
+
+def test_cfg3_full_size(dv):
+    """BASELINE config 3 at full size: all 90,112 circuits vs the oracle (bench launch config)."""
+    _check_workload(dv, configs.cfg3())
+
+
+def test_cfg4_full_size_sampled(dv):
+    """Config 4 (360,448 circuits): strided sample vs the oracle; cost vs oracle aggregation."""
+    w = configs.cfg4()
+    idx = np.arange(0, w.n_circuits, 13)
+    _check_workload(dv, w, idx=idx)
+
+
+def test_batch_equals_single(dv):
+    w = configs.cfg1()
+    ctx = dv.from_workload(w)
+    try:
+        ths = np.stack([w.theta0(s) for s in range(5)])
+        cb, ep = ctx.cost_batch(ths)
+        for k in range(5):
+            c1, E, Psi = ctx.cost(ths[k], with_E_Psi=True)
+            assert abs(cb[k] - c1) <= 1e-14
+            ref = ocost.cost(sim.workload_terms(w, ths[k]), ocost.coeffs_of(w), w.n, w.L)[0]
+            assert abs(cb[k] - ref) <= TOL
+    finally:
+        ctx.destroy()
+
+
+def test_deterministic_bitwise(dv):
+    w = configs.cfg3()
+    ctx = dv.from_workload(w)
+    try:
+        th = w.theta0(3)
+        a = ctx.terms(th)
+        b = ctx.terms(th)
+        assert np.array_equal(a, b)
+        assert ctx.cost(th) == ctx.cost(th)
+    finally:
+        ctx.destroy()
+
+
+def test_special_cases(dv):
+    """l = k denominators are (1, 0); at theta = 0 only zero-x-mask terms survive."""
+    w = configs.cfg1()
+    ctx = dv.from_workload(w)
+    try:
+        g = ctx.terms(np.zeros(w.n_params))
+        ref = sim.workload_terms(w, np.zeros(w.n_params))
+        assert np.max(np.abs(g - ref)) <= TOL
+        n, L = w.n, w.L
+        for l in range(L):
+            t = (l * L + l) * (n + 1)
+            assert abs(g[2 * t] - 1) < 1e-14 and abs(g[2 * t + 1]) < 1e-14
+    finally:
+        ctx.destroy()
+
+
+def test_degenerate_denominator_reported(dv):
+    """All-zero coefficients give Re Psi = 0 <= 1e-12 -> DVQLS_E_DEGENERATE, cost NaN."""
+    ctx = dv.Context(2, 1, b"IXZY", np.zeros(4))
+    try:
+        with pytest.raises(dv.DegenerateError):
+            ctx.cost(np.zeros(6))
+    finally:
+        ctx.destroy()
+
+
+def test_device_resident_entry_point(dv):
+    import torch
+    w = configs.cfg1()
+    ctx = dv.from_workload(w)
+    try:
+        th = torch.tensor(w.theta0(), dtype=torch.float64, device="cuda")
+        out = torch.empty(5, dtype=torch.float64, device="cuda")
+        ctx.cost_dev(1, th, out)
+        torch.cuda.synchronize()
+        torch.cuda.current_stream().synchronize()
+        import ctypes  # noqa: F401
+        dv.load()  # stream sync through the context
+        ctx_c = ctx.cost(w.theta0())
+        assert abs(out[0].item() - ctx_c) < 1e-14
+    finally:
+        ctx.destroy()
