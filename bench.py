@@ -77,19 +77,32 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        self.recording = False
+        self.raw = []
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-i", ",".join(map(str, self.gpus)), "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                                          "-i", ",".join(map(str, self.gpus)), "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.raw and time.time() - t0 < 10:  # wait until sampling is live
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
         return self
 
+    def start(self):
+        self.recording = True
+
+    def stop(self):
+        self.recording = False
+
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.raw.append(line.strip())
+            if self.recording:
+                self.lines.append(line.strip())
 
     def __exit__(self, *a):
         if self.proc:
@@ -116,7 +129,8 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(nm)
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0,
+                    "raw": self.raw[:3]}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
                 "samples": len(sm)}
 
@@ -207,7 +221,7 @@ def run_reference(args, w):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--batch", type=int, default=1, help="thetas per step (dvqls_cost_dev K)")
@@ -268,18 +282,26 @@ def main():
         return float(t.item())
 
     # ---- device-resident timed region ----------------------------------------------------
+    sampler = ClockSampler(list(range(world))) if rank == 0 else None
+    if sampler:
+        sampler.__enter__()
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
+        # W warm-up steps, continued until >= 0.5 s of load so the SM clock has ramped
+        t_w = time.time()
+        i = 0
+        while i < args.warmup or time.time() - t_w < 0.5:
             flush.zero_()
             ctx.cost_dev(KT, th_dev, out_dev)
+            if i % 16 == 15:
+                torch.cuda.synchronize()
+            i += 1
         barrier()
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         kt = []
-        sampler = ClockSampler(list(range(world))) if rank == 0 else None
-        if sampler:
-            sampler.__enter__()
         barrier()
+        if sampler:
+            sampler.start()
         for i in range(args.steps):
             flush.zero_()
             starts[i].record(stream)
@@ -288,7 +310,9 @@ def main():
             kt.append(ctx.last_timings())  # events of the library on the same stream
         barrier()
         if sampler:
-            sampler.__exit__()
+            sampler.stop()
+    if sampler:
+        sampler.__exit__()
     dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     dev_ms = max_over_ranks(dev_ms)
     res = out_dev.view(KT, 5).cpu().numpy()

@@ -43,18 +43,24 @@ KernelCfg make_cfg() {
   k.fn = (const void*)&hadamard_kernel<NQ, W, HH>;
   k.warps = W;
   k.gpw = S::GPW;
-  k.smem = sizeof(double2) * (size_t(HH ? 2 : 1) * S::N + size_t(W) * S::GPW * S::N);
+  k.smem = sizeof(double2) * (size_t(HH ? 3 : 2) * S::N + size_t(W) * S::GPW * S::N) +
+           sizeof(double) * 4 * size_t(W) * S::GPW;
   return k;
 }
 
-// n >= 9 keeps 32 amplitudes per thread: 12 warps (168 registers) or 8 warps
-// (no register cap); DVQLS_WARPS=8 selects the latter (tuning knob).
+// n >= 9 keeps 32 amplitudes per thread (128 registers of branch state).
+// Registers are split per SM sub-partition (16K each), so the choices are 8 warps
+// (2 per scheduler, <= 255 registers) or 12 warps (3 per scheduler, <= 168).
+// Measured on B200 (profiles/): 12 warps is faster for the uniform-b path; the
+// Householder path needs a third N-vector of SMEM and only fits 8.
+// DVQLS_WARPS=8 forces the 8-warp variant (tuning knob).
 template <int NQ, bool HH>
 KernelCfg pick_cfg() {
   if constexpr (NQ >= 9) {
     const char* e = getenv("DVQLS_WARPS");
-    if (e && atoi(e) == 8) return make_cfg<NQ, HH, 8>();
-    return make_cfg<NQ, HH, 12>();
+    const int w = e ? atoi(e) : 12;
+    if (w == 12 && !HH) return make_cfg<NQ, HH, 12>();
+    return make_cfg<NQ, HH, 8>();
   } else {
     return make_cfg<NQ, HH, 16>();
   }
@@ -243,7 +249,7 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
       fail(ctx, DVQLS_E_PAULI, "duplicate Pauli string %s (term %d)", s.c_str(), l);
       return bail(DVQLS_E_PAULI);
     }
-    PauliTerm t{0, 0, 0, 0};
+    PauliTerm t{0, 0, 0, 0u};
     for (int q = 0; q < n; ++q) {
       const uint32_t bit = 1u << (n - 1 - q);
       switch (s[q]) {
@@ -256,6 +262,9 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
           return bail(DVQLS_E_PAULI);
       }
     }
+    // register-part sign word: bit r = popcount(r & (zm >> TB)) & 1, TB = n/2 (kernels.cuh Shape)
+    const uint32_t zh = t.zm >> (n / 2);
+    for (int r = 0; r < 32; ++r) t.wpar |= uint32_t(__builtin_popcount(uint32_t(r) & zh) & 1) << r;
     tab[l] = t;
   }
   std::vector<double2> coef(L);
@@ -337,8 +346,11 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   ctx->grid = int(std::max<int64_t>(1, std::min(want, need)));
   ctx->NG = int64_t(ctx->grid) * groups_per_cta;
 
-  ctx->prefix_threads = std::min(512, std::max(32, ctx->N / 2));
-  ctx->prefix_smem = sizeof(double2) * (2 * size_t(ctx->N) + 4 * size_t(n) * layers);
+  {
+    const int T = ctx->N >> (n >= 2 ? 2 : 1);
+    ctx->prefix_threads = std::min(1024, std::max(32, (T + 31) / 32 * 32));
+  }
+  ctx->prefix_smem = sizeof(double2) * (2 * size_t(ctx->N) + 4 * size_t(n) * layers) + sizeof(int) * ctx->N;
   if (cudaFuncSetAttribute((const void*)&prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(ctx->prefix_smem)) != cudaSuccess) {
     fail(ctx, DVQLS_E_CUDA, "prefix kernel smem %zu B", ctx->prefix_smem);

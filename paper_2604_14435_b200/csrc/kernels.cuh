@@ -24,7 +24,8 @@ namespace dvqls {
 
 struct PauliTerm {  // P|j> = i^{ny} (-1)^{popcount(j & zm)} |j ^ xm>, big-endian masks
   uint32_t xm, zm;
-  int32_t ny, pad;
+  int32_t ny;
+  uint32_t wpar;  // bit r = popcount(r & (zm >> TB)) & 1: register-part sign word (host-built)
 };
 
 // sign flip of a double by XOR of the IEEE sign bit (m = 0 or 0x80000000):
@@ -36,21 +37,36 @@ __device__ __forceinline__ double flip(double v, uint32_t m) {
 // ---------------------------------------------------------------------------
 // a2: shared ansatz prefix.  One CTA per theta; state in SMEM (n <= 12).
 // Each layer: n fused single-qubit unitaries U_q = Ry(t2) Rz(t1) Ry(t0)
-// (within-circuit gate fusion of the three rotations on one qubit), then the
-// entangling ring as ONE index permutation (CNOT) or ONE diagonal sign (CZ).
+// (within-circuit fusion of the three rotations on one qubit), applied two
+// qubits at a time: every thread holds 4 amplitudes in registers (the two
+// index bits of the current qubit pair), so a layer is ceil(n/2) phases of
+// load -> 2 gates -> store into the other SMEM buffer -> one barrier.  The
+// entangling ring is one index permutation (CNOT ring) or one diagonal sign
+// (CZ ring), folded into the first load of the next layer (and the final
+// write-out) through a precomputed table.
 // ---------------------------------------------------------------------------
-__global__ void prefix_kernel(int n, int layers, int entangler, const double* __restrict__ thetas,
-                              double2* __restrict__ x_all) {
+__device__ __forceinline__ double2 cmad2(double2 u0, double2 a, double2 u1, double2 b) {
+  // u0 * a + u1 * b (complex)
+  return make_double2(fma(u0.x, a.x, fma(-u0.y, a.y, fma(u1.x, b.x, -u1.y * b.y))),
+                      fma(u0.x, a.y, fma(u0.y, a.x, fma(u1.x, b.y, u1.y * b.x))));
+}
+
+__global__ void __launch_bounds__(1024)
+prefix_kernel(int n, int layers, int entangler, const double* __restrict__ thetas, double2* __restrict__ x_all) {
   extern __shared__ double2 psm[];
   const int N = 1 << n;
   const int P = 3 * n * layers;
   const int G = n * layers;
-  double2* a = psm;
-  double2* b = psm + N;
-  double2* U = psm + 2 * N;  // 4 entries per fused gate
+  const int rb = n >= 2 ? 2 : 1;
+  const int T = N >> rb;  // active threads
+  double2* bufA = psm;
+  double2* bufB = psm + N;
+  double2* U = psm + 2 * N;                  // 4 entries per fused gate
+  int* perm = reinterpret_cast<int*>(U + 4 * G);  // ring permutation (| sign << 31 for CZ)
   const double* th = thetas + (size_t)blockIdx.x * P;
+  const int tid = threadIdx.x;
 
-  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+  for (int g = tid; g < G; g += blockDim.x) {
     double s0, c0, s1, c1, s2, c2;
     sincos(0.5 * th[3 * g + 0], &s0, &c0);
     sincos(0.5 * th[3 * g + 1], &s1, &c1);
@@ -65,52 +81,89 @@ __global__ void prefix_kernel(int n, int layers, int entangler, const double* __
     U[4 * g + 2] = make_double2(s2 * m00.x + c2 * m10.x, s2 * m00.y + c2 * m10.y);
     U[4 * g + 3] = make_double2(s2 * m01.x + c2 * m11.x, s2 * m01.y + c2 * m11.y);
   }
-  for (int i = threadIdx.x; i < N; i += blockDim.x) a[i] = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
-  __syncthreads();
-
-  for (int layer = 0; layer < layers; ++layer) {
-    for (int q = 0; q < n; ++q) {
-      const int pos = n - 1 - q;
-      const double2 u00 = U[4 * (layer * n + q) + 0], u01 = U[4 * (layer * n + q) + 1];
-      const double2 u10 = U[4 * (layer * n + q) + 2], u11 = U[4 * (layer * n + q) + 3];
-      for (int p = threadIdx.x; p < N / 2; p += blockDim.x) {
-        const int i0 = ((p >> pos) << (pos + 1)) | (p & ((1 << pos) - 1));
-        const int i1 = i0 | (1 << pos);
-        const double2 va = a[i0], vb = a[i1];
-        a[i0] = make_double2(u00.x * va.x - u00.y * va.y + u01.x * vb.x - u01.y * vb.y,
-                             u00.x * va.y + u00.y * va.x + u01.x * vb.y + u01.y * vb.x);
-        a[i1] = make_double2(u10.x * va.x - u10.y * va.y + u11.x * vb.x - u11.y * vb.y,
-                             u10.x * va.y + u10.y * va.x + u11.x * vb.y + u11.y * vb.x);
-      }
-      __syncthreads();
-    }
+  for (int i = tid; i < N; i += blockDim.x) {
+    int e = i;
     if (n >= 2) {
       if (entangler == 0) {
-        // CNOT ring C_{n-1} ... C_0 (C_q: control q -> target (q+1) mod n, C_0 first):
+        // CNOT ring C_{n-1} ... C_0 (C_q: control q -> target (q+1) mod n, C_0 applied first):
         // new[i] = old[c_0(c_1(...c_{n-1}(i)))]
-        for (int i = threadIdx.x; i < N; i += blockDim.x) {
-          int j = i;
-          for (int q = n - 1; q >= 0; --q) {
-            const int pc = n - 1 - q, pt = n - 1 - ((q + 1) % n);
-            if ((j >> pc) & 1) j ^= 1 << pt;
-          }
-          b[i] = a[j];
+        int j = i;
+        for (int q = n - 1; q >= 0; --q) {
+          const int pc = n - 1 - q, pt = n - 1 - ((q + 1) % n);
+          if ((j >> pc) & 1) j ^= 1 << pt;
         }
-        __syncthreads();
-        double2* tmp = a; a = b; b = tmp;
+        e = j;
       } else {
         // CZ ring: diagonal (-1)^{sum_q b_q b_{q+1 mod n}}
-        for (int i = threadIdx.x; i < N; i += blockDim.x) {
-          int par = 0;
-          for (int q = 0; q < n; ++q) par ^= ((i >> (n - 1 - q)) & (i >> (n - 1 - (q + 1) % n))) & 1;
-          if (par) a[i] = make_double2(-a[i].x, -a[i].y);
-        }
-        __syncthreads();
+        int par = 0;
+        for (int q = 0; q < n; ++q) par ^= ((i >> (n - 1 - q)) & (i >> (n - 1 - (q + 1) % n))) & 1;
+        e = int(unsigned(i) | (unsigned(par) << 31));
       }
+    }
+    perm[i] = e;
+    bufA[i] = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+
+  double2* src = bufA;
+  double2* dst = bufB;
+  const int phases = (n + rb - 1) / rb;
+  for (int layer = 0; layer < layers; ++layer) {
+    for (int ph = 0; ph < phases; ++ph) {
+      const int b0 = n >= 2 ? min(2 * ph, n - 2) : 0;  // register bits b0, b0+1
+      if (tid < T) {
+        double2 v[4];
+        int idx[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (r < (1 << rb)) {
+            idx[r] = ((tid >> b0) << (b0 + rb)) | (r << b0) | (tid & ((1 << b0) - 1));
+            if (ph == 0 && layer > 0 && n >= 2) {  // previous layer's entangling ring
+              const int e = perm[idx[r]];
+              double2 a = src[e & 0x7fffffff];
+              if (e < 0) a = make_double2(-a.x, -a.y);
+              v[r] = a;
+            } else {
+              v[r] = src[idx[r]];
+            }
+          }
+        }
+#pragma unroll
+        for (int rbit = 0; rbit < 2; ++rbit) {
+          const int pos = b0 + rbit;
+          if (rbit < rb && pos >= rb * ph) {  // qubit not yet rotated in this layer
+            const int g = layer * n + (n - 1 - pos);
+            const double2 u00 = U[4 * g + 0], u01 = U[4 * g + 1], u10 = U[4 * g + 2], u11 = U[4 * g + 3];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              if (r < (1 << rb) && !(r & (1 << rbit))) {
+                const double2 a = v[r], b = v[r | (1 << rbit)];
+                v[r] = cmad2(u00, a, u01, b);
+                v[r | (1 << rbit)] = cmad2(u10, a, u11, b);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (r < (1 << rb)) dst[idx[r]] = v[r];
+      }
+      __syncthreads();
+      double2* tmp = src; src = dst; dst = tmp;
     }
   }
   double2* x = x_all + (size_t)blockIdx.x * N;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) x[i] = a[i];
+  for (int i = tid; i < N; i += blockDim.x) {
+    double2 a;
+    if (n >= 2) {
+      const int e = perm[i];
+      a = src[e & 0x7fffffff];
+      if (e < 0) a = make_double2(-a.x, -a.y);
+    } else {
+      a = src[i];
+    }
+    x[i] = a;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -161,21 +214,107 @@ __device__ __forceinline__ void fwht_regs(double2 (&v)[R]) {
   }
 }
 
+// A value the compiler cannot see through: stops it from keeping 32 exchange addresses
+// alive between the two exchanges of a circuit (they are one LOP3 each to recompute).
+// (a shuffle with offset 0: ptxas cannot prove the result equal to its input)
+__device__ __forceinline__ uint32_t opaque(uint32_t v, unsigned gmask) {
+  return __shfl_xor_sync(gmask, v, 0);
+}
+
+__host__ __device__ constexpr int ctz_c(int k) {
+  return (k & 1) ? 0 : (k & 2) ? 1 : (k & 4) ? 2 : (k & 8) ? 3 : (k & 16) ? 4 : (k & 32) ? 5 : 6;
+}
+
+// Registers are visited in Gray-code order r_k = k ^ (k >> 1): every index map used here
+// (XOR masks, sign bit, swizzle) is GF(2)-linear in r, so the next address is the
+// previous one XOR one column -- one LOP3 and one live address register per access.
+//
+// Exchange A -> B (A_TO_B) or B -> A through the group's SMEM buffer.  Slot of index i
+// is swz(i); swz is linear, so slot((r << TB) | t) = swz(t) ^ swz(r << TB) and
+// slot((t << RB) | r) = swz(t << RB) ^ r.
 template <int NQ, bool A_TO_B>
 __device__ __forceinline__ void exchange(double2 (&v)[Shape<NQ>::R], double2* buf, int t, unsigned gmask) {
   using S = Shape<NQ>;
+  char* b = reinterpret_cast<char*>(buf);
+  const uint32_t to = opaque(uint32_t(t), gmask);
+  const uint32_t slotA0 = uint32_t(swz<NQ>(int(to))) * 16u;              // layout A, r = 0
+  const uint32_t slotB0 = uint32_t(swz<NQ>(int(to) << S::RB)) * 16u;     // layout B, r = 0
   __syncwarp(gmask);  // previous readers of buf are done
+  {
+    uint32_t a = A_TO_B ? slotA0 : slotB0;
 #pragma unroll
-  for (int r = 0; r < S::R; ++r) {
-    const int i = A_TO_B ? ((r << S::TB) | t) : ((t << S::RB) | r);
-    buf[swz<NQ>(i)] = v[r];
+    for (int k = 0; k < S::R; ++k) {
+      const int r = k ^ (k >> 1);
+      if (k) {
+        const int bb = ctz_c(k);
+        a ^= A_TO_B ? uint32_t(swz<NQ>(1 << (S::TB + bb))) * 16u : (16u << bb);
+      }
+      *reinterpret_cast<double2*>(b + a) = v[r];
+    }
   }
   __syncwarp(gmask);
+  {
+    uint32_t a = A_TO_B ? slotB0 : slotA0;
 #pragma unroll
-  for (int r = 0; r < S::R; ++r) {
-    const int i = A_TO_B ? ((t << S::RB) | r) : ((r << S::TB) | t);
-    v[r] = buf[swz<NQ>(i)];
+    for (int k = 0; k < S::R; ++k) {
+      const int r = k ^ (k >> 1);
+      if (k) {
+        const int bb = ctz_c(k);
+        a ^= A_TO_B ? (16u << bb) : uint32_t(swz<NQ>(1 << (S::TB + bb))) * 16u;
+      }
+      v[r] = *reinterpret_cast<const double2*>(b + a);
+    }
   }
+}
+
+// Signed, XOR-permuted read of [x, -x] in layout A (Gray-code addressing):
+//   register r <- (-1)^{sgn0 ^ parity(r & zh)} x[((r ^ mh) << TB) | tl]
+// (SMEM holds x at [0, N) and -x at [N, 2N): the sign is index bit NQ).
+template <int NQ>
+__device__ __forceinline__ void signed_gather(double2 (&v)[Shape<NQ>::R], const double2* sx, uint32_t mh,
+                                              uint32_t tl, uint32_t zh, uint32_t sgn0) {
+  using S = Shape<NQ>;
+  const char* b = reinterpret_cast<const char*>(sx);
+  uint32_t a = (((mh << S::TB) | tl) | (sgn0 << NQ)) * 16u;
+#pragma unroll
+  for (int k = 0; k < S::R; ++k) {
+    const int r = k ^ (k >> 1);
+    if (k) {
+      const int bb = ctz_c(k);
+      a ^= ((1u << (S::TB + bb)) | (((zh >> bb) & 1u) << NQ)) * 16u;
+    }
+    v[r] = *reinterpret_cast<const double2*>(b + a);
+  }
+}
+
+// Readout sum over registers of conj(x'_r) phi_r, x' from the same signed gather.
+// IM = false: sum Re(conj(x') phi) = xr phr + xi phi;  IM = true: sum Im = xr phi - xi phr.
+template <int NQ, bool IM>
+__device__ __forceinline__ double signed_dot(const double2 (&v)[Shape<NQ>::R], const double2* sx, uint32_t mh,
+                                             uint32_t tl, uint32_t zh, uint32_t sgn0) {
+  using S = Shape<NQ>;
+  const char* b = reinterpret_cast<const char*>(sx);
+  uint32_t a = (((mh << S::TB) | tl) | (sgn0 << NQ)) * 16u;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < S::R; ++k) {
+    const int r = k ^ (k >> 1);
+    if (k) {
+      const int bb = ctz_c(k);
+      a ^= ((1u << (S::TB + bb)) | (((zh >> bb) & 1u) << NQ)) * 16u;
+    }
+    // at most 8 x loads in flight: keeps the live set at 128 branch registers + 32
+    if (k && !(k & 7)) asm volatile("" ::: "memory");
+    const double2 x = *reinterpret_cast<const double2*>(b + a);
+    if (IM) {
+      acc[k & 3] = fma(x.x, v[r].y, acc[k & 3]);
+      acc[k & 3] = fma(-x.y, v[r].x, acc[k & 3]);
+    } else {
+      acc[k & 3] = fma(x.x, v[r].x, acc[k & 3]);
+      acc[k & 3] = fma(x.y, v[r].y, acc[k & 3]);
+    }
+  }
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 template <int GT>
@@ -208,21 +347,47 @@ __device__ __forceinline__ void householder(double2 (&v)[Shape<NQ>::R], const do
   }
 }
 
+// sign flip of every amplitude whose register index has bit B set (compile-time B)
+template <int R, int B>
+__device__ __forceinline__ void zflip_reg(double2 (&v)[R]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (r & (1 << B)) v[r] = make_double2(flip(v[r].x, 0x80000000u), flip(v[r].y, 0x80000000u));
+}
+
+template <int R, int B = 0>
+__device__ __forceinline__ void zflip_reg_rt(double2 (&v)[R], int bit) {
+  if constexpr ((1 << B) < R) {
+    if (bit == B) zflip_reg<R, B>(v);
+    else zflip_reg_rt<R, B + 1>(v, bit);
+  }
+}
+
+// register cap per thread: the whole 64K-entry register file split over WARPS warps,
+// rounded down to the allocation granularity of 8
+template <int WARPS>
+constexpr int reg_cap() { return (65536 / (WARPS * 32)) / 8 * 8 > 255 ? 255 : (65536 / (WARPS * 32)) / 8 * 8; }
+
 template <int NQ, int WARPS, bool HH>
-__global__ void __launch_bounds__(WARPS * 32, 1)
+__global__ void __launch_bounds__(WARPS * 32) __maxnreg__(reg_cap<WARPS>())
 hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ tab,
                 const double2* __restrict__ coef, const double2* __restrict__ hv, double hv_scale, int L,
                 int64_t c0, int64_t C, double* __restrict__ out_terms, double* __restrict__ partials) {
   using S = Shape<NQ>;
   constexpr int TB = S::TB, RB = S::RB, GT = S::GT, R = S::R, N = S::N, GPW = S::GPW;
   extern __shared__ double2 smem[];
-  double2* sx = smem;
-  double2* shv = smem + N;
-  double2* sbuf = smem + (HH ? 2 : 1) * N;
+  double2* sx = smem;              // [x, -x]: 2N
+  double2* shv = smem + 2 * N;     // Householder vector (HH only)
+  double2* sbuf = smem + (HH ? 3 : 2) * N;
+  double* sacc = reinterpret_cast<double*>(sbuf + (size_t)WARPS * GPW * N);  // 4 per group
 
   const int kth = blockIdx.y;  // theta index within a batch
   const double2* x = x_all + (size_t)kth * N;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) sx[i] = x[i];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const double2 a = x[i];
+    sx[i] = a;
+    sx[N + i] = make_double2(-a.x, -a.y);
+  }
   if (HH)
     for (int i = threadIdx.x; i < N; i += blockDim.x) shv[i] = hv[i];
   __syncthreads();
@@ -234,53 +399,46 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
 
   const int64_t NG = (int64_t)gridDim.x * WARPS * GPW;
   const int64_t g = ((int64_t)blockIdx.x * WARPS + warp) * GPW + gw;
-  const int64_t cb = g * C / NG, ce = (g + 1) * C / NG;  // local circuit range
+  const int cb = int(g * C / NG), ce = int((g + 1) * C / NG);  // local circuit range (C < 2^31)
   const int n1 = NQ + 1;
 
-  double Er = 0.0, Ei = 0.0, Pr = 0.0, Pi = 0.0;
-  for (int64_t cl = cb; cl < ce; ++cl) {
+  // per-group running sums (Re E, Im E, Re Psi, Im Psi) live in SMEM, not registers
+  double* acc4 = sacc + 4 * (warp * GPW + gw);
+  if (t == 0) acc4[0] = acc4[1] = acc4[2] = acc4[3] = 0.0;
+  for (int cl = cb; cl < ce; ++cl) {
     const int64_t c = c0 + cl;
     const int64_t tk = c >> 1;
     const int part = int(c & 1);
     const int s = int(tk % n1);
     const int64_t lk = tk / n1;
     const int k = int(lk % L), l = int(lk / L);
-    const PauliTerm Tk = tab[k], Tl = tab[l];
+    const PauliTerm Tk = tab[k];
 
-    // ---- a4: branch init + c-A_k as a signed gather from x (layout A) -----
+    // ---- a4: branch init + c-A_k: phi_i = sgn_k(i ^ m_k) x[i ^ m_k]  (layout A) ----
+    // (the i^{n_Y} and kappa phases are folded into q below)
     double2 v[R];
     {
-      const uint32_t mh = Tk.xm >> TB, ml = Tk.xm & (GT - 1), zh = Tk.zm >> TB, zl = Tk.zm & (GT - 1);
-      const uint32_t ts = __popc((t ^ ml) & zl) & 1;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const uint32_t rr = uint32_t(r) ^ mh;
-        const double2 a = sx[(rr << TB) | (t ^ ml)];
-        const uint32_t sg = ((__popc(rr & zh) & 1) ^ ts) << 31;
-        v[r] = make_double2(flip(a.x, sg), flip(a.y, sg));
-      }
+      const uint32_t mh = Tk.xm >> TB, tl = uint32_t(t) ^ (Tk.xm & (GT - 1)), zh = Tk.zm >> TB;
+      const uint32_t sg0 = (__popc(tl & Tk.zm & (GT - 1)) ^ __popc(mh & zh)) & 1u;
+      signed_gather<NQ>(v, sx, mh, tl, zh, sg0);
     }
     double scale = 1.0;
     if (s > 0) {
       const int p = NQ - 1 - (s - 1);  // bit position of Z_j, j = s - 1
       if (!HH) {
-        // ---- a5: c-U_b^+ = unnormalised FWHT ------------------------------
+        // ---- a5: c-U_b^+ = unnormalised FWHT (layout A bits TB..NQ-1, layout B bits 0..TB-1)
         fwht_regs<R, 0, RB>(v);
         exchange<NQ, true>(v, buf, t, gmask);
         fwht_regs<R, 0, TB>(v);
-        // ---- a6: c-Z_j (layout B) -------------------------------------------
+        // ---- a6: c-Z_j (layout B: register bit p, or thread bit p - RB) --------------
         if (p < RB) {
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const uint32_t m = uint32_t((r >> p) & 1) << 31;
-            v[r] = make_double2(flip(v[r].x, m), flip(v[r].y, m));
-          }
+          zflip_reg_rt<R>(v, p);
         } else {
           const uint32_t m = uint32_t((t >> (p - RB)) & 1) << 31;
 #pragma unroll
           for (int r = 0; r < R; ++r) v[r] = make_double2(flip(v[r].x, m), flip(v[r].y, m));
         }
-        // ---- a7: c-U_b ------------------------------------------------------
+        // ---- a7: c-U_b ------------------------------------------------------------------
         fwht_regs<R, 0, TB>(v);
         exchange<NQ, false>(v, buf, t, gmask);
         fwht_regs<R, 0, RB>(v);
@@ -288,11 +446,7 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
       } else {
         householder<NQ>(v, shv, hv_scale, t, gmask);
         if (p >= TB) {
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const uint32_t m = uint32_t((r >> (p - TB)) & 1) << 31;
-            v[r] = make_double2(flip(v[r].x, m), flip(v[r].y, m));
-          }
+          zflip_reg_rt<R>(v, p - TB);
         } else {
           const uint32_t m = uint32_t((t >> p) & 1) << 31;
 #pragma unroll
@@ -301,35 +455,16 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
         householder<NQ>(v, shv, hv_scale, t, gmask);
       }
     }
-    // ---- a8: c-A_l + ancilla readout, Re(i^q S) with S = sum_j conj(x_{j^m}) sgn_l(j) phi_j
+    // ---- a8: c-A_l + ancilla readout: Re(i^q S), S = sum_j conj(sgn_l(j) x_{j ^ m_l}) phi_j
+    const PauliTerm Tl = tab[l];  // loaded late: not live across the FWHTs
     const int q = (Tk.ny + Tl.ny + 3 * part) & 3;
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    double val;
     {
-      const uint32_t mh = Tl.xm >> TB, ml = Tl.xm & (GT - 1), zh = Tl.zm >> TB, zl = Tl.zm & (GT - 1);
-      const uint32_t ts = __popc(t & zl) & 1;
-      if (q & 1) {  // Im S = sum (xr phi_i - xi phi_r)
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const double2 a = sx[((uint32_t(r) ^ mh) << TB) | (t ^ ml)];
-          const uint32_t sg = ((__popc(uint32_t(r) & zh) & 1) ^ ts) << 31;
-          const double xr = flip(a.x, sg), xi = flip(a.y, sg ^ 0x80000000u);
-          double& acc = (r & 3) == 0 ? acc0 : (r & 3) == 1 ? acc1 : (r & 3) == 2 ? acc2 : acc3;
-          acc = fma(xr, v[r].y, acc);
-          acc = fma(xi, v[r].x, acc);
-        }
-      } else {  // Re S = sum (xr phi_r + xi phi_i)
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const double2 a = sx[((uint32_t(r) ^ mh) << TB) | (t ^ ml)];
-          const uint32_t sg = ((__popc(uint32_t(r) & zh) & 1) ^ ts) << 31;
-          const double xr = flip(a.x, sg), xi = flip(a.y, sg);
-          double& acc = (r & 3) == 0 ? acc0 : (r & 3) == 1 ? acc1 : (r & 3) == 2 ? acc2 : acc3;
-          acc = fma(xr, v[r].x, acc);
-          acc = fma(xi, v[r].y, acc);
-        }
-      }
+      const uint32_t mh = Tl.xm >> TB, tl = uint32_t(t) ^ (Tl.xm & (GT - 1)), zh = Tl.zm >> TB;
+      const uint32_t sg0 = __popc(uint32_t(t) & Tl.zm & (GT - 1)) & 1u;
+      val = (q & 1) ? signed_dot<NQ, true>(v, sx, mh, tl, zh, sg0) : signed_dot<NQ, false>(v, sx, mh, tl, zh, sg0);
     }
-    double val = group_sum<GT>((acc0 + acc1) + (acc2 + acc3), gmask);
+    val = group_sum<GT>(val, gmask);
     val *= (q == 1 || q == 2) ? -scale : scale;
 
     // ---- a9 (fused): write the term, accumulate c_l^* c_k (Re + i Im) -----
@@ -339,12 +474,14 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
       const double wr = cl_.x * ck.x + cl_.y * ck.y, wi = cl_.x * ck.y - cl_.y * ck.x;
       const double cr = part == 0 ? wr * val : -wi * val;
       const double ci = part == 0 ? wi * val : wr * val;
-      if (s == 0) { Pr += cr; Pi += ci; } else { Er += cr; Ei += ci; }
+      double* d = acc4 + (s == 0 ? 2 : 0);
+      d[0] += cr;
+      d[1] += ci;
     }
   }
   if (t == 0) {
     double* o = partials + ((size_t)kth * NG + g) * 4;
-    o[0] = Er; o[1] = Ei; o[2] = Pr; o[3] = Pi;
+    o[0] = acc4[0]; o[1] = acc4[1]; o[2] = acc4[2]; o[3] = acc4[3];
   }
 }
 
