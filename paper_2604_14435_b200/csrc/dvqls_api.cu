@@ -98,6 +98,8 @@ struct dvqls_ctx {
   int grid = 0;     // CTAs per theta
   int64_t NG = 0;   // circuit groups per theta
   int prefix_threads = 0;
+  int prefix_rb = 3;
+  const void* prefix_fn = nullptr;
   size_t prefix_smem = 0;
   double hv_scale = 0.0;
 
@@ -150,9 +152,11 @@ thread_local std::string g_create_err;
 
 int launch_eval(dvqls_ctx* ctx, int K, const double* thetas_dev, bool want_cost, double* out_dev) {
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-  prefix_kernel<<<K, ctx->prefix_threads, ctx->prefix_smem, ctx->stream>>>(ctx->n, ctx->layers, ctx->entangler,
-                                                                            thetas_dev, ctx->d_x);
-  CK(cudaGetLastError());
+  {
+    void* args[] = {(void*)&ctx->n, (void*)&ctx->layers, (void*)&ctx->entangler, (void*)&thetas_dev,
+                    (void*)&ctx->d_x};
+    CK(cudaLaunchKernel(ctx->prefix_fn, dim3(K), dim3(ctx->prefix_threads), args, ctx->prefix_smem, ctx->stream));
+  }
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], ctx->stream));
   const int64_t Cloc = ctx->c1 - ctx->c0;
   {
@@ -346,12 +350,15 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   ctx->grid = int(std::max<int64_t>(1, std::min(want, need)));
   ctx->NG = int64_t(ctx->grid) * groups_per_cta;
 
+  ctx->prefix_rb = std::min(3, n);
+  ctx->prefix_fn = ctx->prefix_rb == 3 ? (const void*)&prefix_kernel<3>
+                   : ctx->prefix_rb == 2 ? (const void*)&prefix_kernel<2> : (const void*)&prefix_kernel<1>;
   {
-    const int T = ctx->N >> (n >= 2 ? 2 : 1);
-    ctx->prefix_threads = std::min(1024, std::max(32, (T + 31) / 32 * 32));
+    const int T = ctx->N >> ctx->prefix_rb;
+    ctx->prefix_threads = std::min(512, std::max(32, (T + 31) / 32 * 32));
   }
-  ctx->prefix_smem = sizeof(double2) * (2 * size_t(ctx->N) + 4 * size_t(n) * layers) + sizeof(int) * ctx->N;
-  if (cudaFuncSetAttribute((const void*)&prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  ctx->prefix_smem = sizeof(double2) * (2 * size_t(ctx->N) + 2 * size_t(n) * layers) + sizeof(int) * ctx->N;
+  if (cudaFuncSetAttribute(ctx->prefix_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(ctx->prefix_smem)) != cudaSuccess) {
     fail(ctx, DVQLS_E_CUDA, "prefix kernel smem %zu B", ctx->prefix_smem);
     return bail(DVQLS_E_CUDA);

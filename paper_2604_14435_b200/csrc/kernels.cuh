@@ -36,33 +36,29 @@ __device__ __forceinline__ double flip(double v, uint32_t m) {
 
 // ---------------------------------------------------------------------------
 // a2: shared ansatz prefix.  One CTA per theta; state in SMEM (n <= 12).
-// Each layer: n fused single-qubit unitaries U_q = Ry(t2) Rz(t1) Ry(t0)
-// (within-circuit fusion of the three rotations on one qubit), applied two
-// qubits at a time: every thread holds 4 amplitudes in registers (the two
-// index bits of the current qubit pair), so a layer is ceil(n/2) phases of
-// load -> 2 gates -> store into the other SMEM buffer -> one barrier.  The
+// Each layer applies n fused single-qubit unitaries U_q = Ry(t2) Rz(t1) Ry(t0)
+// (within-circuit fusion of the three rotations on one qubit; U_q is in SU(2),
+// U = [[a, -conj(b)], [b, conj(a)]], so a gate is two complex numbers), RB
+// qubits at a time: every thread holds 2^RB amplitudes in registers (the RB
+// index bits of the current qubit group), so a layer is ceil(n/RB) phases of
+// load -> RB gates -> store into the other SMEM buffer -> one barrier.  The
 // entangling ring is one index permutation (CNOT ring) or one diagonal sign
 // (CZ ring), folded into the first load of the next layer (and the final
 // write-out) through a precomputed table.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double2 cmad2(double2 u0, double2 a, double2 u1, double2 b) {
-  // u0 * a + u1 * b (complex)
-  return make_double2(fma(u0.x, a.x, fma(-u0.y, a.y, fma(u1.x, b.x, -u1.y * b.y))),
-                      fma(u0.x, a.y, fma(u0.y, a.x, fma(u1.x, b.y, u1.y * b.x))));
-}
-
-__global__ void __launch_bounds__(1024)
+template <int RB>
+__global__ void __launch_bounds__(512)
 prefix_kernel(int n, int layers, int entangler, const double* __restrict__ thetas, double2* __restrict__ x_all) {
+  constexpr int RA = 1 << RB;
   extern __shared__ double2 psm[];
   const int N = 1 << n;
   const int P = 3 * n * layers;
   const int G = n * layers;
-  const int rb = n >= 2 ? 2 : 1;
-  const int T = N >> rb;  // active threads
+  const int T = N >> RB;  // active threads
   double2* bufA = psm;
   double2* bufB = psm + N;
-  double2* U = psm + 2 * N;                  // 4 entries per fused gate
-  int* perm = reinterpret_cast<int*>(U + 4 * G);  // ring permutation (| sign << 31 for CZ)
+  double2* U = psm + 2 * N;                       // (a, b) per fused gate
+  int* perm = reinterpret_cast<int*>(U + 2 * G);  // ring permutation (| sign << 31 for CZ)
   const double* th = thetas + (size_t)blockIdx.x * P;
   const int tid = threadIdx.x;
 
@@ -71,15 +67,10 @@ prefix_kernel(int n, int layers, int entangler, const double* __restrict__ theta
     sincos(0.5 * th[3 * g + 0], &s0, &c0);
     sincos(0.5 * th[3 * g + 1], &s1, &c1);
     sincos(0.5 * th[3 * g + 2], &s2, &c2);
-    // M = Rz(t1) Ry(t0) = [[e0 c0, -e0 s0], [e1 s0, e1 c0]], e0 = e^{-i t1/2}, e1 = e^{+i t1/2}
-    const double2 e0 = make_double2(c1, -s1), e1 = make_double2(c1, s1);
-    const double2 m00 = make_double2(e0.x * c0, e0.y * c0), m01 = make_double2(-e0.x * s0, -e0.y * s0);
-    const double2 m10 = make_double2(e1.x * s0, e1.y * s0), m11 = make_double2(e1.x * c0, e1.y * c0);
-    // U = Ry(t2) M = [[c2 m00 - s2 m10, c2 m01 - s2 m11], [s2 m00 + c2 m10, s2 m01 + c2 m11]]
-    U[4 * g + 0] = make_double2(c2 * m00.x - s2 * m10.x, c2 * m00.y - s2 * m10.y);
-    U[4 * g + 1] = make_double2(c2 * m01.x - s2 * m11.x, c2 * m01.y - s2 * m11.y);
-    U[4 * g + 2] = make_double2(s2 * m00.x + c2 * m10.x, s2 * m00.y + c2 * m10.y);
-    U[4 * g + 3] = make_double2(s2 * m01.x + c2 * m11.x, s2 * m01.y + c2 * m11.y);
+    // Rz(t1) Ry(t0) = [[e0 c0, -e0 s0], [e1 s0, e1 c0]], e0 = e^{-i t1/2}, e1 = e^{+i t1/2};
+    // U = Ry(t2) Rz(t1) Ry(t0): a = U00 = c2 e0 c0 - s2 e1 s0, b = U10 = s2 e0 c0 + c2 e1 s0
+    U[2 * g + 0] = make_double2(c1 * (c2 * c0 - s2 * s0), -s1 * (c2 * c0 + s2 * s0));
+    U[2 * g + 1] = make_double2(c1 * (s2 * c0 + c2 * s0), s1 * (c2 * s0 - s2 * c0));
   }
   for (int i = tid; i < N; i += blockDim.x) {
     int e = i;
@@ -107,46 +98,46 @@ prefix_kernel(int n, int layers, int entangler, const double* __restrict__ theta
 
   double2* src = bufA;
   double2* dst = bufB;
-  const int phases = (n + rb - 1) / rb;
+  const int phases = (n + RB - 1) / RB;
   for (int layer = 0; layer < layers; ++layer) {
     for (int ph = 0; ph < phases; ++ph) {
-      const int b0 = n >= 2 ? min(2 * ph, n - 2) : 0;  // register bits b0, b0+1
+      const int b0 = min(RB * ph, n - RB);  // register bits b0 .. b0+RB-1
       if (tid < T) {
-        double2 v[4];
-        int idx[4];
+        const int base = ((tid >> b0) << (b0 + RB)) | (tid & ((1 << b0) - 1));
+        double2 v[RA];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          if (r < (1 << rb)) {
-            idx[r] = ((tid >> b0) << (b0 + rb)) | (r << b0) | (tid & ((1 << b0) - 1));
-            if (ph == 0 && layer > 0 && n >= 2) {  // previous layer's entangling ring
-              const int e = perm[idx[r]];
-              double2 a = src[e & 0x7fffffff];
-              if (e < 0) a = make_double2(-a.x, -a.y);
-              v[r] = a;
-            } else {
-              v[r] = src[idx[r]];
-            }
+        for (int r = 0; r < RA; ++r) {
+          const int idx = base | (r << b0);
+          if (ph == 0 && layer > 0) {  // previous layer's entangling ring
+            const int e = perm[idx];
+            double2 a = src[e & 0x7fffffff];
+            if (e < 0) a = make_double2(-a.x, -a.y);
+            v[r] = a;
+          } else {
+            v[r] = src[idx];
           }
         }
 #pragma unroll
-        for (int rbit = 0; rbit < 2; ++rbit) {
+        for (int rbit = 0; rbit < RB; ++rbit) {
           const int pos = b0 + rbit;
-          if (rbit < rb && pos >= rb * ph) {  // qubit not yet rotated in this layer
+          if (pos >= RB * ph) {  // qubit not yet rotated in this layer
             const int g = layer * n + (n - 1 - pos);
-            const double2 u00 = U[4 * g + 0], u01 = U[4 * g + 1], u10 = U[4 * g + 2], u11 = U[4 * g + 3];
+            const double2 ua = U[2 * g + 0], ub = U[2 * g + 1];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              if (r < (1 << rb) && !(r & (1 << rbit))) {
-                const double2 a = v[r], b = v[r | (1 << rbit)];
-                v[r] = cmad2(u00, a, u01, b);
-                v[r | (1 << rbit)] = cmad2(u10, a, u11, b);
+            for (int r = 0; r < RA; ++r) {
+              if (!(r & (1 << rbit))) {
+                const double2 x0 = v[r], x1 = v[r | (1 << rbit)];
+                // y0 = a x0 - conj(b) x1 ; y1 = b x0 + conj(a) x1
+                v[r] = make_double2(fma(ua.x, x0.x, fma(-ua.y, x0.y, fma(-ub.x, x1.x, -ub.y * x1.y))),
+                                    fma(ua.x, x0.y, fma(ua.y, x0.x, fma(-ub.x, x1.y, ub.y * x1.x))));
+                v[r | (1 << rbit)] = make_double2(fma(ub.x, x0.x, fma(-ub.y, x0.y, fma(ua.x, x1.x, ua.y * x1.y))),
+                                                  fma(ub.x, x0.y, fma(ub.y, x0.x, fma(ua.x, x1.y, -ua.y * x1.x))));
               }
             }
           }
         }
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (r < (1 << rb)) dst[idx[r]] = v[r];
+        for (int r = 0; r < RA; ++r) dst[base | (r << b0)] = v[r];
       }
       __syncthreads();
       double2* tmp = src; src = dst; dst = tmp;
