@@ -152,7 +152,10 @@ thread_local std::string g_create_err;
 
 int launch_eval(dvqls_ctx* ctx, int K, const double* thetas_dev, bool want_cost, double* out_dev) {
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-  {
+  if (ctx->prefix_rb == 0) {
+    void* args[] = {(void*)&ctx->layers, (void*)&ctx->entangler, (void*)&thetas_dev, (void*)&ctx->d_x};
+    CK(cudaLaunchKernel(ctx->prefix_fn, dim3(K), dim3(ctx->prefix_threads), args, ctx->prefix_smem, ctx->stream));
+  } else {
     void* args[] = {(void*)&ctx->n, (void*)&ctx->layers, (void*)&ctx->entangler, (void*)&thetas_dev,
                     (void*)&ctx->d_x};
     CK(cudaLaunchKernel(ctx->prefix_fn, dim3(K), dim3(ctx->prefix_threads), args, ctx->prefix_smem, ctx->stream));
@@ -350,14 +353,27 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   ctx->grid = int(std::max<int64_t>(1, std::min(want, need)));
   ctx->NG = int64_t(ctx->grid) * groups_per_cta;
 
-  ctx->prefix_rb = std::min(3, n);
-  ctx->prefix_fn = ctx->prefix_rb == 3 ? (const void*)&prefix_kernel<3>
-                   : ctx->prefix_rb == 2 ? (const void*)&prefix_kernel<2> : (const void*)&prefix_kernel<1>;
   {
+    const char* e = getenv("DVQLS_PREFIX_RB");  // tuning knob: register-phase prefix for n <= 10
+    ctx->prefix_rb = e ? std::min(std::max(1, std::min(3, atoi(e))), n) : (n <= 10 ? 0 : std::min(3, n));
+  }
+  if (ctx->prefix_rb == 0) {  // one amplitude per thread, shuffles + 2 transposes per layer
+    static const void* lanes[11] = {nullptr,
+                                    (const void*)&prefix_lanes_kernel<1>, (const void*)&prefix_lanes_kernel<2>,
+                                    (const void*)&prefix_lanes_kernel<3>, (const void*)&prefix_lanes_kernel<4>,
+                                    (const void*)&prefix_lanes_kernel<5>, (const void*)&prefix_lanes_kernel<6>,
+                                    (const void*)&prefix_lanes_kernel<7>, (const void*)&prefix_lanes_kernel<8>,
+                                    (const void*)&prefix_lanes_kernel<9>, (const void*)&prefix_lanes_kernel<10>};
+    ctx->prefix_fn = lanes[n];
+    ctx->prefix_threads = std::max(32, ctx->N);
+    ctx->prefix_smem = sizeof(double2) * (size_t(ctx->N) + 4 * size_t(n) * layers) + sizeof(int) * ctx->N;
+  } else {
+    ctx->prefix_fn = ctx->prefix_rb == 3 ? (const void*)&prefix_kernel<3>
+                     : ctx->prefix_rb == 2 ? (const void*)&prefix_kernel<2> : (const void*)&prefix_kernel<1>;
     const int T = ctx->N >> ctx->prefix_rb;
     ctx->prefix_threads = std::min(512, std::max(32, (T + 31) / 32 * 32));
+    ctx->prefix_smem = sizeof(double2) * (2 * size_t(ctx->N) + 2 * size_t(n) * layers) + sizeof(int) * ctx->N;
   }
-  ctx->prefix_smem = sizeof(double2) * (2 * size_t(ctx->N) + 2 * size_t(n) * layers) + sizeof(int) * ctx->N;
   if (cudaFuncSetAttribute(ctx->prefix_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(ctx->prefix_smem)) != cudaSuccess) {
     fail(ctx, DVQLS_E_CUDA, "prefix kernel smem %zu B", ctx->prefix_smem);

@@ -46,6 +46,11 @@ __device__ __forceinline__ double flip(double v, uint32_t m) {
 // (CZ ring), folded into the first load of the next layer (and the final
 // write-out) through a precomputed table.
 // ---------------------------------------------------------------------------
+// SMEM slot of state index i in the prefix: XOR-swizzle of the low 3 bits with bits 3..5,
+// so every register-group phase hits 8 distinct 16-byte bank groups per quarter warp
+// (without it the phase whose qubits are the low index bits is 2^RB-way conflicted).
+__device__ __forceinline__ int pswz(int i) { return i ^ ((i >> 3) & 7); }
+
 template <int RB>
 __global__ void __launch_bounds__(512)
 prefix_kernel(int n, int layers, int entangler, const double* __restrict__ thetas, double2* __restrict__ x_all) {
@@ -92,7 +97,7 @@ prefix_kernel(int n, int layers, int entangler, const double* __restrict__ theta
       }
     }
     perm[i] = e;
-    bufA[i] = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
+    bufA[pswz(i)] = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
   }
   __syncthreads();
 
@@ -110,11 +115,11 @@ prefix_kernel(int n, int layers, int entangler, const double* __restrict__ theta
           const int idx = base | (r << b0);
           if (ph == 0 && layer > 0) {  // previous layer's entangling ring
             const int e = perm[idx];
-            double2 a = src[e & 0x7fffffff];
+            double2 a = src[pswz(e & 0x7fffffff)];
             if (e < 0) a = make_double2(-a.x, -a.y);
             v[r] = a;
           } else {
-            v[r] = src[idx];
+            v[r] = src[pswz(idx)];
           }
         }
 #pragma unroll
@@ -137,7 +142,7 @@ prefix_kernel(int n, int layers, int entangler, const double* __restrict__ theta
           }
         }
 #pragma unroll
-        for (int r = 0; r < RA; ++r) dst[base | (r << b0)] = v[r];
+        for (int r = 0; r < RA; ++r) dst[pswz(base | (r << b0))] = v[r];
       }
       __syncthreads();
       double2* tmp = src; src = dst; dst = tmp;
@@ -148,13 +153,116 @@ prefix_kernel(int n, int layers, int entangler, const double* __restrict__ theta
     double2 a;
     if (n >= 2) {
       const int e = perm[i];
-      a = src[e & 0x7fffffff];
+      a = src[pswz(e & 0x7fffffff)];
       if (e < 0) a = make_double2(-a.x, -a.y);
     } else {
-      a = src[i];
+      a = src[pswz(i)];
     }
     x[i] = a;
   }
+}
+
+// ---------------------------------------------------------------------------
+// a2 for n <= 10: one amplitude per thread (2^n threads, up to 32 warps).
+// Index i is split into LB = min(5, n) lane bits and WB = n - LB warp bits.
+//   layout X: i = (w << LB) | l   -> gates on positions [0, LB) are lane bits
+//   layout Y: i = (l << WB) | w   -> gates on positions [LB, n) are lane bits
+// A gate on a lane bit is one shuffle of the partner amplitude and one complex
+// 2-term dot (8 FP64 ops per amplitude, no redundant work); the row of U a thread
+// needs (c_self, c_other) is read from a per-gate table by the thread's bit.
+// A layer is X-gates, transpose X->Y, Y-gates, transpose Y->X with the
+// entangling ring folded into the read, i.e. two barriers per layer.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int tswz(int i) { return i ^ ((i >> 5) & 7); }
+
+template <int NQ>
+__global__ void __launch_bounds__(1024)
+prefix_lanes_kernel(int layers, int entangler, const double* __restrict__ thetas, double2* __restrict__ x_all) {
+  constexpr int n = NQ;
+  constexpr int N = 1 << n;
+  constexpr int LB = n < 5 ? n : 5, WB = n - LB;
+  extern __shared__ double2 qsm[];
+  const int P = 3 * n * layers;
+  const int G = n * layers;
+  double2* sbuf = qsm;                            // N amplitudes (transposes)
+  double2* tabU = qsm + N;                        // 4 per gate: [bit0: c_self, c_other, bit1: ...]
+  int* perm = reinterpret_cast<int*>(tabU + 4 * G);
+  const double* th = thetas + (size_t)blockIdx.x * P;
+  const int tid = threadIdx.x;
+  const int l = tid & 31, w = tid >> 5;
+  const unsigned full = 0xffffffffu;
+
+  for (int g = tid; g < G; g += blockDim.x) {
+    double s0, c0, s1, c1, s2, c2;
+    sincos(0.5 * th[3 * g + 0], &s0, &c0);
+    sincos(0.5 * th[3 * g + 1], &s1, &c1);
+    sincos(0.5 * th[3 * g + 2], &s2, &c2);
+    // U = Ry(t2) Rz(t1) Ry(t0) = [[a, -conj(b)], [b, conj(a)]]
+    const double2 a = make_double2(c1 * (c2 * c0 - s2 * s0), -s1 * (c2 * c0 + s2 * s0));
+    const double2 b = make_double2(c1 * (s2 * c0 + c2 * s0), s1 * (c2 * s0 - s2 * c0));
+    tabU[4 * g + 0] = a;                             // bit 0: self  = U00
+    tabU[4 * g + 1] = make_double2(-b.x, b.y);       // bit 0: other = U01 = -conj(b)
+    tabU[4 * g + 2] = make_double2(a.x, -a.y);       // bit 1: self  = U11 = conj(a)
+    tabU[4 * g + 3] = b;                             // bit 1: other = U10 = b
+  }
+  for (int i = tid; i < N; i += blockDim.x) {
+    int e = i;
+    if (n >= 2) {
+      if (entangler == 0) {
+        int j = i;  // new[i] = old[c_0(c_1(...c_{n-1}(i)))]
+#pragma unroll
+        for (int q = n - 1; q >= 0; --q) {
+          const int pc = n - 1 - q, pt = n - 1 - ((q + 1) % n);
+          if ((j >> pc) & 1) j ^= 1 << pt;
+        }
+        e = j;
+      } else {
+        int par = 0;
+#pragma unroll
+        for (int q = 0; q < n; ++q) par ^= ((i >> (n - 1 - q)) & (i >> (n - 1 - (q + 1) % n))) & 1;
+        e = int(unsigned(i) | (unsigned(par) << 31));
+      }
+    }
+    perm[i] = e;
+  }
+  __syncthreads();
+
+  const bool active = tid < N;
+  const int ixX = (w << LB) | l, ixY = (l << WB) | w;
+  const int sX = tswz(ixX), sY = tswz(ixY);
+  const int eperm = (active && n >= 2) ? perm[ixX] : ixX;
+  const int sP = tswz(eperm & 0x7fffffff);
+  const bool pneg = eperm < 0;
+  double2 v = make_double2(tid == 0 ? 1.0 : 0.0, 0.0);  // layout X, |0...0>
+  for (int layer = 0; layer < layers; ++layer) {
+    // gate table of this layer: qubit q = n - 1 - pos at tabU + 4 (layer n + q) + 2 mybit
+    const double2* tl = tabU + 4 * (layer * n) + 2 * 0;
+#pragma unroll
+    for (int pos = 0; pos < n; ++pos) {
+      if (pos == LB && WB > 0) {  // X -> Y transpose
+        if (active) sbuf[sX] = v;
+        __syncthreads();
+        if (active) v = sbuf[sY];
+        __syncthreads();
+      }
+      const int lbit = pos < LB ? pos : pos - WB;  // lane bit carrying this position
+      const int mybit = (l >> lbit) & 1;
+      const double2* u = tl + 4 * (n - 1 - pos) + 2 * mybit;
+      const double2 cs = u[0], co = u[1];
+      const double2 pp = make_double2(__shfl_xor_sync(full, v.x, 1 << lbit), __shfl_xor_sync(full, v.y, 1 << lbit));
+      v = make_double2(fma(cs.x, v.x, fma(-cs.y, v.y, fma(co.x, pp.x, -co.y * pp.y))),
+                       fma(cs.x, v.y, fma(cs.y, v.x, fma(co.x, pp.y, co.y * pp.x))));
+    }
+    // back to layout X with the entangling ring folded into the read
+    if (active) sbuf[WB > 0 ? sY : sX] = v;
+    __syncthreads();
+    if (active) {
+      const double2 a = sbuf[sP];
+      v = pneg ? make_double2(-a.x, -a.y) : a;
+    }
+    __syncthreads();
+  }
+  if (active) x_all[(size_t)blockIdx.x * N + ixX] = v;
 }
 
 // ---------------------------------------------------------------------------

@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 TAG=${TAG:-iter}
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest.log 2>&1
 timeout 300 python bench.py --no-cpu-baseline > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
-for W in 8; do DVQLS_WARPS=$W timeout 300 python bench.py --no-cpu-baseline > gpurun_out/${TAG}_bench_w$W.json 2>&1; done
+#for W in 8; do DVQLS_WARPS=$W timeout 300 python bench.py --no-cpu-baseline > gpurun_out/${TAG}_bench_w$W.json 2>&1; done
 B="python bench.py --steps 5 --warmup 3 --no-cpu-baseline"
 if [ "${NCU:-1}" = "1" ]; then
 timeout 300 $B > gpurun_out/${TAG}_b5.json 2>&1 && \
