@@ -130,6 +130,11 @@ int dvqls_cost_dev(dvqls_ctx* ctx, int K, const double* thetas_dev, double* out_
  *   out_dev  (c1 - c0) doubles in device memory */
 int dvqls_terms_local_dev(dvqls_ctx* ctx, const double* theta_dev, double* out_dev);
 
+/* Solution state |x(theta)> = V(theta)|0> (Alg. 1 Step 5), computed by the
+ * prefix kernel and copied to the host.
+ *   out_state  2*2^n doubles, interleaved (re, im), big-endian index order. */
+int dvqls_state(dvqls_ctx* ctx, const double* theta, double* out_state);
+
 /* ---- introspection ------------------------------------------------------ */
 const char* dvqls_last_error(const dvqls_ctx* ctx); /* "" if none; static text if ctx NULL */
 int64_t dvqls_num_circuits(const dvqls_ctx* ctx);   /* 2(n+1)L^2 */

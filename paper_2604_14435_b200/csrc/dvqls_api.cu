@@ -507,6 +507,25 @@ int dvqls_terms(dvqls_ctx* ctx, const double* theta, double* out) {
   return DVQLS_OK;
 }
 
+int dvqls_state(dvqls_ctx* ctx, const double* theta, double* out_state) {
+  if (!ctx) return DVQLS_E_ARG;
+  ctx->err.clear();
+  if (!theta || !out_state) return fail(ctx, DVQLS_E_ARG, "NULL host pointer");
+  std::memcpy(ctx->h_stage, theta, sizeof(double) * ctx->P);
+  CK(cudaMemcpyAsync(ctx->d_theta, ctx->h_stage, sizeof(double) * ctx->P, cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->prefix_rb == 0) {
+    void* args[] = {(void*)&ctx->layers, (void*)&ctx->entangler, (void*)&ctx->d_theta, (void*)&ctx->d_x};
+    CK(cudaLaunchKernel(ctx->prefix_fn, dim3(1), dim3(ctx->prefix_threads), args, ctx->prefix_smem, ctx->stream));
+  } else {
+    void* args[] = {(void*)&ctx->n, (void*)&ctx->layers, (void*)&ctx->entangler, (void*)&ctx->d_theta,
+                    (void*)&ctx->d_x};
+    CK(cudaLaunchKernel(ctx->prefix_fn, dim3(1), dim3(ctx->prefix_threads), args, ctx->prefix_smem, ctx->stream));
+  }
+  CK(cudaMemcpyAsync(out_state, ctx->d_x, sizeof(double2) * ctx->N, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DVQLS_OK;
+}
+
 const char* dvqls_last_error(const dvqls_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_create_err.c_str();
 }

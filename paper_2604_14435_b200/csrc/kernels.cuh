@@ -28,6 +28,18 @@ struct PauliTerm {  // P|j> = i^{ny} (-1)^{popcount(j & zm)} |j ^ xm>, big-endia
   uint32_t wpar;  // bit r = popcount(r & (zm >> TB)) & 1: register-part sign word (host-built)
 };
 
+// Dynamic shared memory of the Hadamard-test kernel.  Accesses are written as
+// byte offsets from this symbol so the compiler folds the base into the
+// LDS/STS immediate and the per-access address work is a single XOR.
+extern __shared__ double2 dvqls_smem[];
+
+__device__ __forceinline__ double2 lds2(uint32_t off) {
+  return *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(dvqls_smem) + off);
+}
+__device__ __forceinline__ void sts2(uint32_t off, double2 v) {
+  *reinterpret_cast<double2*>(reinterpret_cast<char*>(dvqls_smem) + off) = v;
+}
+
 // sign flip of a double by XOR of the IEEE sign bit (m = 0 or 0x80000000):
 // one ALU LOP3 on the high word, no FP64-pipe instruction.
 __device__ __forceinline__ double flip(double v, uint32_t m) {
@@ -332,12 +344,13 @@ __host__ __device__ constexpr int ctz_c(int k) {
 // is swz(i); swz is linear, so slot((r << TB) | t) = swz(t) ^ swz(r << TB) and
 // slot((t << RB) | r) = swz(t << RB) ^ r.
 template <int NQ, bool A_TO_B>
-__device__ __forceinline__ void exchange(double2 (&v)[Shape<NQ>::R], double2* buf, int t, unsigned gmask) {
+__device__ __forceinline__ void exchange(double2 (&v)[Shape<NQ>::R], uint32_t buf_off, int t, unsigned gmask) {
   using S = Shape<NQ>;
-  char* b = reinterpret_cast<char*>(buf);
+  // buf_off is a multiple of the buffer size (a power of two >= every slot offset),
+  // so buf_off + slot == buf_off ^ slot and the whole address is one XOR chain.
   const uint32_t to = opaque(uint32_t(t), gmask);
-  const uint32_t slotA0 = uint32_t(swz<NQ>(int(to))) * 16u;              // layout A, r = 0
-  const uint32_t slotB0 = uint32_t(swz<NQ>(int(to) << S::RB)) * 16u;     // layout B, r = 0
+  const uint32_t slotA0 = buf_off ^ (uint32_t(swz<NQ>(int(to))) * 16u);           // layout A, r = 0
+  const uint32_t slotB0 = buf_off ^ (uint32_t(swz<NQ>(int(to) << S::RB)) * 16u);  // layout B, r = 0
   __syncwarp(gmask);  // previous readers of buf are done
   {
     uint32_t a = A_TO_B ? slotA0 : slotB0;
@@ -348,7 +361,7 @@ __device__ __forceinline__ void exchange(double2 (&v)[Shape<NQ>::R], double2* bu
         const int bb = ctz_c(k);
         a ^= A_TO_B ? uint32_t(swz<NQ>(1 << (S::TB + bb))) * 16u : (16u << bb);
       }
-      *reinterpret_cast<double2*>(b + a) = v[r];
+      sts2(a, v[r]);
     }
   }
   __syncwarp(gmask);
@@ -361,7 +374,7 @@ __device__ __forceinline__ void exchange(double2 (&v)[Shape<NQ>::R], double2* bu
         const int bb = ctz_c(k);
         a ^= A_TO_B ? (16u << bb) : uint32_t(swz<NQ>(1 << (S::TB + bb))) * 16u;
       }
-      v[r] = *reinterpret_cast<const double2*>(b + a);
+      v[r] = lds2(a);
     }
   }
 }
@@ -370,10 +383,9 @@ __device__ __forceinline__ void exchange(double2 (&v)[Shape<NQ>::R], double2* bu
 //   register r <- (-1)^{sgn0 ^ parity(r & zh)} x[((r ^ mh) << TB) | tl]
 // (SMEM holds x at [0, N) and -x at [N, 2N): the sign is index bit NQ).
 template <int NQ>
-__device__ __forceinline__ void signed_gather(double2 (&v)[Shape<NQ>::R], const double2* sx, uint32_t mh,
-                                              uint32_t tl, uint32_t zh, uint32_t sgn0) {
+__device__ __forceinline__ void signed_gather(double2 (&v)[Shape<NQ>::R], uint32_t mh, uint32_t tl, uint32_t zh,
+                                              uint32_t sgn0) {
   using S = Shape<NQ>;
-  const char* b = reinterpret_cast<const char*>(sx);
   uint32_t a = (((mh << S::TB) | tl) | (sgn0 << NQ)) * 16u;
 #pragma unroll
   for (int k = 0; k < S::R; ++k) {
@@ -382,17 +394,16 @@ __device__ __forceinline__ void signed_gather(double2 (&v)[Shape<NQ>::R], const 
       const int bb = ctz_c(k);
       a ^= ((1u << (S::TB + bb)) | (((zh >> bb) & 1u) << NQ)) * 16u;
     }
-    v[r] = *reinterpret_cast<const double2*>(b + a);
+    v[r] = lds2(a);
   }
 }
 
 // Readout sum over registers of conj(x'_r) phi_r, x' from the same signed gather.
 // IM = false: sum Re(conj(x') phi) = xr phr + xi phi;  IM = true: sum Im = xr phi - xi phr.
 template <int NQ, bool IM>
-__device__ __forceinline__ double signed_dot(const double2 (&v)[Shape<NQ>::R], const double2* sx, uint32_t mh,
-                                             uint32_t tl, uint32_t zh, uint32_t sgn0) {
+__device__ __forceinline__ double signed_dot(const double2 (&v)[Shape<NQ>::R], uint32_t mh, uint32_t tl,
+                                             uint32_t zh, uint32_t sgn0) {
   using S = Shape<NQ>;
-  const char* b = reinterpret_cast<const char*>(sx);
   uint32_t a = (((mh << S::TB) | tl) | (sgn0 << NQ)) * 16u;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -404,7 +415,7 @@ __device__ __forceinline__ double signed_dot(const double2 (&v)[Shape<NQ>::R], c
     }
     // at most 8 x loads in flight: keeps the live set at 128 branch registers + 32
     if (k && !(k & 7)) asm volatile("" ::: "memory");
-    const double2 x = *reinterpret_cast<const double2*>(b + a);
+    const double2 x = lds2(a);
     if (IM) {
       acc[k & 3] = fma(x.x, v[r].y, acc[k & 3]);
       acc[k & 3] = fma(-x.y, v[r].x, acc[k & 3]);
@@ -474,7 +485,7 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
                 int64_t c0, int64_t C, double* __restrict__ out_terms, double* __restrict__ partials) {
   using S = Shape<NQ>;
   constexpr int TB = S::TB, RB = S::RB, GT = S::GT, R = S::R, N = S::N, GPW = S::GPW;
-  extern __shared__ double2 smem[];
+  double2* smem = dvqls_smem;
   double2* sx = smem;              // [x, -x]: 2N
   double2* shv = smem + 2 * N;     // Householder vector (HH only)
   double2* sbuf = smem + (HH ? 3 : 2) * N;
@@ -495,6 +506,8 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
   const int gw = lane / GT, t = lane % GT;
   const unsigned gmask = (GT == 32) ? 0xffffffffu : (((1u << GT) - 1u) << (gw * GT));
   double2* buf = sbuf + (size_t)(warp * GPW + gw) * N;
+  // byte offset of this group's exchange buffer; a multiple of 16 N when HH is false
+  const uint32_t buf_off = uint32_t(reinterpret_cast<char*>(buf) - reinterpret_cast<char*>(smem));
 
   const int64_t NG = (int64_t)gridDim.x * WARPS * GPW;
   const int64_t g = ((int64_t)blockIdx.x * WARPS + warp) * GPW + gw;
@@ -519,7 +532,7 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
     {
       const uint32_t mh = Tk.xm >> TB, tl = uint32_t(t) ^ (Tk.xm & (GT - 1)), zh = Tk.zm >> TB;
       const uint32_t sg0 = (__popc(tl & Tk.zm & (GT - 1)) ^ __popc(mh & zh)) & 1u;
-      signed_gather<NQ>(v, sx, mh, tl, zh, sg0);
+      signed_gather<NQ>(v, mh, tl, zh, sg0);
     }
     double scale = 1.0;
     if (s > 0) {
@@ -527,7 +540,7 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
       if (!HH) {
         // ---- a5: c-U_b^+ = unnormalised FWHT (layout A bits TB..NQ-1, layout B bits 0..TB-1)
         fwht_regs<R, 0, RB>(v);
-        exchange<NQ, true>(v, buf, t, gmask);
+        exchange<NQ, true>(v, buf_off, t, gmask);
         fwht_regs<R, 0, TB>(v);
         // ---- a6: c-Z_j (layout B: register bit p, or thread bit p - RB) --------------
         if (p < RB) {
@@ -539,7 +552,7 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
         }
         // ---- a7: c-U_b ------------------------------------------------------------------
         fwht_regs<R, 0, TB>(v);
-        exchange<NQ, false>(v, buf, t, gmask);
+        exchange<NQ, false>(v, buf_off, t, gmask);
         fwht_regs<R, 0, RB>(v);
         scale = 1.0 / double(N);
       } else {
@@ -561,7 +574,7 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
     {
       const uint32_t mh = Tl.xm >> TB, tl = uint32_t(t) ^ (Tl.xm & (GT - 1)), zh = Tl.zm >> TB;
       const uint32_t sg0 = __popc(uint32_t(t) & Tl.zm & (GT - 1)) & 1u;
-      val = (q & 1) ? signed_dot<NQ, true>(v, sx, mh, tl, zh, sg0) : signed_dot<NQ, false>(v, sx, mh, tl, zh, sg0);
+      val = (q & 1) ? signed_dot<NQ, true>(v, mh, tl, zh, sg0) : signed_dot<NQ, false>(v, mh, tl, zh, sg0);
     }
     val = group_sum<GT>(val, gmask);
     val *= (q == 1 || q == 2) ? -scale : scale;

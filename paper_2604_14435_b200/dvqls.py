@@ -30,7 +30,7 @@ EXPORTED = [
     "dvqls_create", "dvqls_destroy", "dvqls_terms", "dvqls_cost", "dvqls_cost_batch",
     "dvqls_cost_dev", "dvqls_terms_local_dev", "dvqls_last_error", "dvqls_num_circuits",
     "dvqls_local_range", "dvqls_stream", "dvqls_launches_per_call", "dvqls_last_timings",
-    "dvqls_nccl_unique_id", "dvqls_build_info", "dvqls_shard_range",
+    "dvqls_nccl_unique_id", "dvqls_build_info", "dvqls_shard_range", "dvqls_state",
 ]
 
 
@@ -76,6 +76,7 @@ def load():
     L.dvqls_cost_batch.argtypes = [vp, ctypes.c_int, dp, dp, dp]
     L.dvqls_cost_dev.argtypes = [vp, ctypes.c_int, vp, vp]
     L.dvqls_terms_local_dev.argtypes = [vp, vp, vp]
+    L.dvqls_state.argtypes = [vp, dp, dp]
     L.dvqls_last_error.argtypes = [vp]
     L.dvqls_last_error.restype = ctypes.c_char_p
     L.dvqls_num_circuits.argtypes = [vp]
@@ -188,6 +189,13 @@ class Context:
         ep = np.empty(4 * K)
         _check(load().dvqls_cost_batch(self.h, K, _dp(th), _dp(c), _dp(ep)), self.h)
         return c, ep.reshape(K, 4)
+
+    def state(self, theta) -> np.ndarray:
+        """|x(theta)> = V(theta)|0> from the GPU prefix kernel (Alg. 1 Step 5)."""
+        th = self._theta(theta, 1)
+        out = np.empty(2 << self.n, dtype=np.float64)
+        _check(load().dvqls_state(self.h, _dp(th), _dp(out)), self.h)
+        return out.view(np.complex128)
 
     # --- device-resident entry points (torch tensors or raw pointers) --------
     def cost_dev(self, K, thetas_dev, out_dev):
