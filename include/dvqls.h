@@ -86,7 +86,8 @@ typedef struct dvqls_ctx dvqls_ctx;
  * C = 2(n+1)L^2 circuits ("strided workload allocation"; a contiguous
  * block balances equally) and, for world > 1, create the NCCL
  * communicator.  Collective over all ranks when world > 1.
- *   n_qubits    system qubits n, 1 <= n <= 10 in this build (else UNSUPPORTED)
+ *   n_qubits    system qubits n, 1 <= n <= 24 (n <= 10: register path; 11..12: SMEM
+ *               tile path; 13..24: global streaming path; amplitude b only for n <= 12)
  *   layers      ansatz depth d >= 1; theta has P = 3*n*layers doubles
  *   n_terms     L >= 1
  *   pauli_terms L*n characters, row-major (term l at pauli_terms + l*n)
@@ -134,6 +135,13 @@ int dvqls_terms_local_dev(dvqls_ctx* ctx, const double* theta_dev, double* out_d
  * prefix kernel and copied to the host.
  *   out_state  2*2^n doubles, interleaved (re, im), big-endian index order. */
 int dvqls_state(dvqls_ctx* ctx, const double* theta, double* out_state);
+
+/* Term expectations of a subset of circuits (testing at large n, where evaluating all
+ * 2(n+1)L^2 circuits takes minutes).  Synchronous; single-rank contexts evaluate only the
+ * listed circuits, multi-rank contexts evaluate all and select.
+ *   idx   count circuit indices in [0, 2(n+1)L^2), host memory
+ *   out   count doubles, out[i] = <Z_anc> of circuit idx[i] */
+int dvqls_terms_subset(dvqls_ctx* ctx, const double* theta, const int64_t* idx, int64_t count, double* out);
 
 /* ---- introspection ------------------------------------------------------ */
 const char* dvqls_last_error(const dvqls_ctx* ctx); /* "" if none; static text if ctx NULL */

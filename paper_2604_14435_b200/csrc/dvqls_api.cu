@@ -21,13 +21,16 @@
 
 #include "../../include/dvqls.h"
 #include "kernels.cuh"
+#include "tile.cuh"
 #include "nccl_dl.h"
 
 using namespace dvqls;
 
 namespace {
 
-constexpr int kMaxQubits = 10;  // SMEM-resident path of this build
+constexpr int kMaxRegQubits = 10;  // register-resident path (one circuit per warp or less)
+constexpr int kMaxQubits = 24;     // tile path: SMEM tile (n <= 12) or global streaming (n <= 24)
+constexpr size_t kScratchBudget = size_t(48) << 30;  // bytes of per-CTA branch scratch (n > 12)
 
 struct KernelCfg {
   const void* fn = nullptr;
@@ -114,6 +117,13 @@ struct dvqls_ctx {
   double* d_out = nullptr;       // max_batch * 5
   double* d_gather = nullptr;    // world * chunk (terms allgather)
   double* h_stage = nullptr;     // pinned staging
+  bool tile_path = false;        // n > 10
+  double2* d_scratch = nullptr;  // grid * N (n > 12)
+  double2* d_x2 = nullptr;       // ring ping-pong buffer (n > 12 prefix)
+  double2* d_gates = nullptr;    // fused-gate table (n > 12 prefix)
+  int64_t* d_cidx = nullptr;     // circuit subset (dvqls_terms_subset)
+  double* d_sub = nullptr;
+  int64_t sub_cap = 0;
   size_t h_stage_bytes = 0;
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -150,9 +160,52 @@ int fail(dvqls_ctx* c, int code, const char* fmt, ...) {
 
 thread_local std::string g_create_err;
 
+// Hadamard-test kernel over circuits [c0, c0 + C) (or the list cidx[0..C)) of every theta.
+int launch_hadamard(dvqls_ctx* ctx, int K, int64_t c0, int64_t C, const int64_t* cidx, double* terms, int grid) {
+  dim3 g(grid, K);
+  if (!ctx->tile_path) {
+    void* args[] = {(void*)&ctx->d_x,   (void*)&ctx->d_tab, (void*)&ctx->d_coef,  (void*)&ctx->d_hv,
+                    (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&c0, (void*)&C,
+                    (void*)&terms, (void*)&ctx->d_partials};
+    CK(cudaLaunchKernel(ctx->kc.fn, g, dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
+  } else {
+    void* args[] = {(void*)&ctx->d_x, (void*)&ctx->d_tab, (void*)&ctx->d_coef, (void*)&ctx->d_hv,
+                    (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&ctx->n, (void*)&c0, (void*)&C,
+                    (void*)&cidx, (void*)&ctx->d_scratch, (void*)&terms, (void*)&ctx->d_partials};
+    CK(cudaLaunchKernel(ctx->kc.fn, g, dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
+  }
+  return DVQLS_OK;
+}
+
+// n > 12: V(theta)|0> in global memory, one launch per pass (tile.cuh)
+int launch_prefix_global(dvqls_ctx* ctx, int K, const double* thetas_dev) {
+  const int n = ctx->n, G = n * ctx->layers;
+  const uint32_t N = uint32_t(ctx->N);
+  const int ng = n <= 12 ? 1 : (n <= 21 ? 2 : 3);
+  for (int k = 0; k < K; ++k) {
+    double2* x = ctx->d_x + size_t(k) * N;
+    double2* y = ctx->d_x2;
+    tile::prefix_gates_kernel<<<(G + 127) / 128, 128, 0, ctx->stream>>>(thetas_dev + size_t(k) * ctx->P, G,
+                                                                           ctx->d_gates);
+    tile::prefix_init_kernel<<<1024, 256, 0, ctx->stream>>>(x, N);
+    for (int layer = 0; layer < ctx->layers; ++layer) {
+      for (int gi = 0; gi < ng; ++gi)
+        tile::prefix_gate_pass<<<N >> tile::TBITS, tile::THREADS, sizeof(double2) * tile::TN, ctx->stream>>>(
+            x, ctx->d_gates, n, gi, layer);
+      tile::prefix_ring_kernel<<<1024, 256, 0, ctx->stream>>>(x, y, n, ctx->entangler);
+      CK(cudaMemcpyAsync(x, y, sizeof(double2) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    CK(cudaGetLastError());
+  }
+  return DVQLS_OK;
+}
+
 int launch_eval(dvqls_ctx* ctx, int K, const double* thetas_dev, bool want_cost, double* out_dev) {
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-  if (ctx->prefix_rb == 0) {
+  if (ctx->prefix_rb < 0) {
+    int rc = launch_prefix_global(ctx, K, thetas_dev);
+    if (rc) return rc;
+  } else if (ctx->prefix_rb == 0) {
     void* args[] = {(void*)&ctx->layers, (void*)&ctx->entangler, (void*)&thetas_dev, (void*)&ctx->d_x};
     CK(cudaLaunchKernel(ctx->prefix_fn, dim3(K), dim3(ctx->prefix_threads), args, ctx->prefix_smem, ctx->stream));
   } else {
@@ -163,11 +216,8 @@ int launch_eval(dvqls_ctx* ctx, int K, const double* thetas_dev, bool want_cost,
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], ctx->stream));
   const int64_t Cloc = ctx->c1 - ctx->c0;
   {
-    dim3 grid(ctx->grid, K);
-    void* args[] = {(void*)&ctx->d_x,   (void*)&ctx->d_tab, (void*)&ctx->d_coef,  (void*)&ctx->d_hv,
-                    (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&ctx->c0, (void*)&Cloc,
-                    (void*)&ctx->d_terms, (void*)&ctx->d_partials};
-    CK(cudaLaunchKernel(ctx->kc.fn, grid, dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
+    int rc = launch_hadamard(ctx, K, ctx->c0, Cloc, nullptr, ctx->d_terms, ctx->grid);
+    if (rc) return rc;
   }
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
   if (want_cost) {
@@ -194,6 +244,7 @@ void release(dvqls_ctx* c) {
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
   cudaFree(c->d_tab); cudaFree(c->d_coef); cudaFree(c->d_hv); cudaFree(c->d_theta); cudaFree(c->d_x);
   cudaFree(c->d_terms); cudaFree(c->d_partials); cudaFree(c->d_ep); cudaFree(c->d_out); cudaFree(c->d_gather);
+  cudaFree(c->d_scratch); cudaFree(c->d_x2); cudaFree(c->d_gates); cudaFree(c->d_cidx); cudaFree(c->d_sub);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -217,7 +268,9 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   if (layers < 1) return early(DVQLS_E_ARG, "layers must be >= 1");
   if (L < 1) return early(DVQLS_E_ARG, "n_terms must be >= 1");
   if (!paulis || !coeffs) return early(DVQLS_E_ARG, "pauli_terms / coeffs is NULL");
-  if (n > kMaxQubits) return early(DVQLS_E_UNSUPPORTED, "this build evaluates n <= 10 (SMEM-resident path)");
+  if (n > kMaxQubits) return early(DVQLS_E_UNSUPPORTED, "this build evaluates n <= 24");
+  if (n > 12 && bprep && bprep->kind == DVQLS_B_AMPLITUDES)
+    return early(DVQLS_E_UNSUPPORTED, "amplitude b (Householder U_b) is implemented for n <= 12");
 
   ctx = new dvqls_ctx();
   ctx->n = n; ctx->layers = layers; ctx->L = L; ctx->P = 3 * n * layers; ctx->N = 1 << n;
@@ -330,7 +383,16 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
     }
     ctx->own_stream = true;
   }
-  ctx->kc = ctx->bkind == DVQLS_B_AMPLITUDES ? cfg_for<true>(n) : cfg_for<false>(n);
+  ctx->tile_path = n > kMaxRegQubits;
+  if (!ctx->tile_path) {
+    ctx->kc = ctx->bkind == DVQLS_B_AMPLITUDES ? cfg_for<true>(n) : cfg_for<false>(n);
+  } else {
+    ctx->kc.fn = ctx->bkind == DVQLS_B_AMPLITUDES ? (const void*)&tile::tile_hadamard_kernel<true>
+                                                  : (const void*)&tile::tile_hadamard_kernel<false>;
+    ctx->kc.warps = tile::THREADS / 32;
+    ctx->kc.gpw = 1;
+    ctx->kc.smem = sizeof(double2) * tile::TN;
+  }
   if (cudaFuncSetAttribute(ctx->kc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->kc.smem)) !=
       cudaSuccess) {
     fail(ctx, DVQLS_E_CUDA, "cannot reserve %zu B of shared memory", ctx->kc.smem);
@@ -347,8 +409,12 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   dvqls_shard_range(ctx->C, ctx->rank, ctx->world, &ctx->c0, &ctx->c1);
   ctx->chunk = (ctx->C + ctx->world - 1) / ctx->world;
   const int64_t Cloc = ctx->c1 - ctx->c0;
-  const int64_t groups_per_cta = int64_t(ctx->kc.warps) * ctx->kc.gpw;
+  const int64_t groups_per_cta = ctx->tile_path ? 1 : int64_t(ctx->kc.warps) * ctx->kc.gpw;
   int64_t want = int64_t(prop.multiProcessorCount) * occ;
+  if (ctx->tile_path && n > 12) {  // each CTA owns a 2^n-amplitude global scratch
+    const int64_t cap = int64_t(kScratchBudget / (sizeof(double2) * size_t(ctx->N)));
+    want = std::max<int64_t>(1, std::min(want, cap));
+  }
   const int64_t need = (Cloc + groups_per_cta - 1) / groups_per_cta;
   ctx->grid = int(std::max<int64_t>(1, std::min(want, need)));
   ctx->NG = int64_t(ctx->grid) * groups_per_cta;
@@ -357,7 +423,15 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
     const char* e = getenv("DVQLS_PREFIX_RB");  // tuning knob: register-phase prefix for n <= 10
     ctx->prefix_rb = e ? std::min(std::max(1, std::min(3, atoi(e))), n) : (n <= 10 ? 0 : std::min(3, n));
   }
-  if (ctx->prefix_rb == 0) {  // one amplitude per thread, shuffles + 2 transposes per layer
+  if (n > 12) {
+    ctx->prefix_rb = -1;  // global-memory multi-pass prefix (tile.cuh)
+    ctx->prefix_fn = nullptr;
+    if (cudaFuncSetAttribute((const void*)&tile::prefix_gate_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(sizeof(double2) * tile::TN)) != cudaSuccess) {
+      fail(ctx, DVQLS_E_CUDA, "prefix_gate_pass smem");
+      return bail(DVQLS_E_CUDA);
+    }
+  } else if (ctx->prefix_rb == 0) {  // one amplitude per thread, shuffles + 2 transposes per layer
     static const void* lanes[11] = {nullptr,
                                     (const void*)&prefix_lanes_kernel<1>, (const void*)&prefix_lanes_kernel<2>,
                                     (const void*)&prefix_lanes_kernel<3>, (const void*)&prefix_lanes_kernel<4>,
@@ -374,8 +448,8 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
     ctx->prefix_threads = std::min(512, std::max(32, (T + 31) / 32 * 32));
     ctx->prefix_smem = sizeof(double2) * (2 * size_t(ctx->N) + 2 * size_t(n) * layers) + sizeof(int) * ctx->N;
   }
-  if (cudaFuncSetAttribute(ctx->prefix_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(ctx->prefix_smem)) != cudaSuccess) {
+  if (ctx->prefix_fn && cudaFuncSetAttribute(ctx->prefix_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(ctx->prefix_smem)) != cudaSuccess) {
     fail(ctx, DVQLS_E_CUDA, "prefix kernel smem %zu B", ctx->prefix_smem);
     return bail(DVQLS_E_CUDA);
   }
@@ -390,7 +464,10 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
       alloc((void**)&ctx->d_terms, sizeof(double) * KB * ctx->chunk) ||
       alloc((void**)&ctx->d_partials, sizeof(double) * KB * ctx->NG * 4) ||
       alloc((void**)&ctx->d_ep, sizeof(double) * KB * 4) || alloc((void**)&ctx->d_out, sizeof(double) * KB * 5) ||
-      (ctx->world > 1 && alloc((void**)&ctx->d_gather, sizeof(double) * ctx->world * ctx->chunk))) {
+      (ctx->world > 1 && alloc((void**)&ctx->d_gather, sizeof(double) * ctx->world * ctx->chunk)) ||
+      (n > 12 && alloc((void**)&ctx->d_scratch, sizeof(double2) * size_t(ctx->grid) * ctx->N)) ||
+      (n > 12 && alloc((void**)&ctx->d_x2, sizeof(double2) * size_t(ctx->N))) ||
+      (n > 12 && alloc((void**)&ctx->d_gates, sizeof(double2) * 2 * size_t(n) * layers))) {
     fail(ctx, DVQLS_E_CUDA, "cudaMalloc failed");
     return bail(DVQLS_E_CUDA);
   }
@@ -513,7 +590,10 @@ int dvqls_state(dvqls_ctx* ctx, const double* theta, double* out_state) {
   if (!theta || !out_state) return fail(ctx, DVQLS_E_ARG, "NULL host pointer");
   std::memcpy(ctx->h_stage, theta, sizeof(double) * ctx->P);
   CK(cudaMemcpyAsync(ctx->d_theta, ctx->h_stage, sizeof(double) * ctx->P, cudaMemcpyHostToDevice, ctx->stream));
-  if (ctx->prefix_rb == 0) {
+  if (ctx->prefix_rb < 0) {
+    int rc = launch_prefix_global(ctx, 1, ctx->d_theta);
+    if (rc) return rc;
+  } else if (ctx->prefix_rb == 0) {
     void* args[] = {(void*)&ctx->layers, (void*)&ctx->entangler, (void*)&ctx->d_theta, (void*)&ctx->d_x};
     CK(cudaLaunchKernel(ctx->prefix_fn, dim3(1), dim3(ctx->prefix_threads), args, ctx->prefix_smem, ctx->stream));
   } else {
@@ -522,6 +602,46 @@ int dvqls_state(dvqls_ctx* ctx, const double* theta, double* out_state) {
     CK(cudaLaunchKernel(ctx->prefix_fn, dim3(1), dim3(ctx->prefix_threads), args, ctx->prefix_smem, ctx->stream));
   }
   CK(cudaMemcpyAsync(out_state, ctx->d_x, sizeof(double2) * ctx->N, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DVQLS_OK;
+}
+
+int dvqls_terms_subset(dvqls_ctx* ctx, const double* theta, const int64_t* idx, int64_t count, double* out) {
+  if (!ctx) return DVQLS_E_ARG;
+  ctx->err.clear();
+  if (!theta || !out || (count > 0 && !idx) || count < 0) return fail(ctx, DVQLS_E_ARG, "bad subset arguments");
+  for (int64_t i = 0; i < count; ++i)
+    if (idx[i] < 0 || idx[i] >= ctx->C) return fail(ctx, DVQLS_E_ARG, "circuit index %lld out of range", (long long)idx[i]);
+  if (count == 0) return DVQLS_OK;
+  if (!ctx->tile_path || ctx->world > 1) {  // evaluate everything, pick the requested entries
+    std::vector<double> all(size_t(ctx->C));
+    int rc = dvqls_terms(ctx, theta, all.data());
+    if (rc) return rc;
+    for (int64_t i = 0; i < count; ++i) out[i] = all[size_t(idx[i])];
+    return DVQLS_OK;
+  }
+  if (count > ctx->sub_cap) {
+    cudaFree(ctx->d_cidx); cudaFree(ctx->d_sub);
+    ctx->d_cidx = nullptr; ctx->d_sub = nullptr; ctx->sub_cap = 0;
+    CK(cudaMalloc((void**)&ctx->d_cidx, sizeof(int64_t) * count));
+    CK(cudaMalloc((void**)&ctx->d_sub, sizeof(double) * count));
+    ctx->sub_cap = count;
+  }
+  std::memcpy(ctx->h_stage, theta, sizeof(double) * ctx->P);
+  CK(cudaMemcpyAsync(ctx->d_theta, ctx->h_stage, sizeof(double) * ctx->P, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_cidx, idx, sizeof(int64_t) * count, cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->prefix_rb < 0) {
+    int rc = launch_prefix_global(ctx, 1, ctx->d_theta);
+    if (rc) return rc;
+  } else {
+    void* args[] = {(void*)&ctx->n, (void*)&ctx->layers, (void*)&ctx->entangler, (void*)&ctx->d_theta,
+                    (void*)&ctx->d_x};
+    CK(cudaLaunchKernel(ctx->prefix_fn, dim3(1), dim3(ctx->prefix_threads), args, ctx->prefix_smem, ctx->stream));
+  }
+  const int grid = int(std::min<int64_t>(ctx->grid, count));
+  int rc = launch_hadamard(ctx, 1, 0, count, ctx->d_cidx, ctx->d_sub, grid);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(out, ctx->d_sub, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return DVQLS_OK;
 }
@@ -574,7 +694,8 @@ int dvqls_shard_range(int64_t n_circuits, int rank, int world, int64_t* c0, int6
 }
 
 const char* dvqls_build_info(void) {
-  return "libdvqls sm_100a; SMEM-resident Hadamard-test path n=1..10; fp64 (complex128); NCCL via dlopen";
+  return "libdvqls sm_100a; register-resident Hadamard-test path n=1..10, SMEM-tile path n=11..12, "
+         "global streaming path n=13..24; fp64 (complex128); NCCL via dlopen";
 }
 
 }  // extern "C"

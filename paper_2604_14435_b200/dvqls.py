@@ -31,6 +31,7 @@ EXPORTED = [
     "dvqls_cost_dev", "dvqls_terms_local_dev", "dvqls_last_error", "dvqls_num_circuits",
     "dvqls_local_range", "dvqls_stream", "dvqls_launches_per_call", "dvqls_last_timings",
     "dvqls_nccl_unique_id", "dvqls_build_info", "dvqls_shard_range", "dvqls_state",
+    "dvqls_terms_subset",
 ]
 
 
@@ -77,6 +78,7 @@ def load():
     L.dvqls_cost_dev.argtypes = [vp, ctypes.c_int, vp, vp]
     L.dvqls_terms_local_dev.argtypes = [vp, vp, vp]
     L.dvqls_state.argtypes = [vp, dp, dp]
+    L.dvqls_terms_subset.argtypes = [vp, dp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64, dp]
     L.dvqls_last_error.argtypes = [vp]
     L.dvqls_last_error.restype = ctypes.c_char_p
     L.dvqls_num_circuits.argtypes = [vp]
@@ -189,6 +191,14 @@ class Context:
         ep = np.empty(4 * K)
         _check(load().dvqls_cost_batch(self.h, K, _dp(th), _dp(c), _dp(ep)), self.h)
         return c, ep.reshape(K, 4)
+
+    def terms_subset(self, theta, idx) -> np.ndarray:
+        th = self._theta(theta, 1)
+        ix = np.ascontiguousarray(idx, dtype=np.int64)
+        out = np.empty(ix.size, dtype=np.float64)
+        _check(load().dvqls_terms_subset(self.h, _dp(th), ix.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                         ix.size, _dp(out)), self.h)
+        return out
 
     def state(self, theta) -> np.ndarray:
         """|x(theta)> = V(theta)|0> from the GPU prefix kernel (Alg. 1 Step 5)."""

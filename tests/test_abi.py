@@ -57,8 +57,11 @@ def test_argument_errors_without_device(lib):
     assert _create(lib, n=0)[0] == dvqls.DVQLS_E_ARG
     assert _create(lib, n=25, paulis=b"I" * 25)[0] == dvqls.DVQLS_E_ARG
     assert _create(lib, layers=0)[0] == dvqls.DVQLS_E_ARG
-    rc, msg = _create(lib, n=11, paulis=b"I" * 11)
-    assert rc == dvqls.DVQLS_E_UNSUPPORTED and "n <= 10" in msg
+    amps = np.zeros(2 << 13)
+    amps[0] = 1.0
+    bp13 = dvqls._BPrep(1, amps.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    rc, msg = _create(lib, n=13, paulis=b"I" * 13, bprep=ctypes.byref(bp13))
+    assert rc == dvqls.DVQLS_E_UNSUPPORTED and "n <= 12" in msg
     rc, msg = _create(lib, paulis=b"IXQY")
     assert rc == dvqls.DVQLS_E_PAULI and "bad Pauli" in msg
     rc, msg = _create(lib, paulis=b"IXIX")
