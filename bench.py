@@ -37,7 +37,7 @@ sys.path.insert(0, ROOT)
 
 from dvqls_inputs import configs  # noqa: E402
 
-CONFIGS = {"cfg1": configs.cfg1, "cfg3": configs.cfg3, "cfg4": configs.cfg4}
+CONFIGS = {"cfg1": configs.cfg1, "cfg3": configs.cfg3, "cfg4": configs.cfg4, "cfg5": configs.cfg5}
 METRIC = "Hadamard-test circuits/sec & cost evals/sec, 10q 90,112 circuits, 1/2/4/8 B200"
 L2_FLUSH_BYTES = 256 << 20
 
@@ -53,6 +53,13 @@ def fp64_ops_per_eval(w, circuits=None):
     num = int(np.count_nonzero(s))
     den = c.size - num
     return num * (4 * w.n + 2) * N + den * 2 * N
+
+
+def hbm_bytes_per_eval(w, circuits=None):
+    """Streaming-path algorithmic HBM bytes (SURVEY §8(d) "streaming model", n > 12):
+    numerator circuit 3 passes = 96 N B (P1 reads x / writes phi, P2 reads+writes phi,
+    P3 reads phi and x), denominator 32 N B."""
+    return smem_bytes_per_eval(w, circuits)
 
 
 def smem_bytes_per_eval(w, circuits=None):
@@ -151,6 +158,17 @@ def traffic_from_profiles():
     return None
 
 
+def streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src):
+    b = hbm_bytes_per_eval(w, local_c) * KT
+    ach = b / (had_ms * 1e-3)
+    peak = float(peaks["hbm_gbs"]) * 1e9
+    return {"bound": "hbm", "kernel": "tile_hadamard_kernel", "achieved": ach / 1e9, "peak": peak / 1e9,
+            "unit": "GB/s", "frac": ach / peak, "traffic": None,
+            "note": (f"algorithmic HBM bytes per launch = {b:.4g} (96N per numerator circuit, 32N per "
+                     f"denominator, SURVEY §8(d) streaming model) / mean CUDA-event kernel time; peak = "
+                     f"hbm_gbs of {peak_src} MEASURED_PEAKS.json; n > 21 runs 5 passes (160N)")}
+
+
 # ----------------------------------------------------------------------------------------------
 def cpu_baseline(w, theta, budget_s=12.0):
     """Oracle (as it stands) on all host cores, bounded strided samples of the workload."""
@@ -225,11 +243,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--batch", type=int, default=1, help="thetas per step (dvqls_cost_dev K)")
+    ap.add_argument("--n", type=int, default=16, help="qubits for --config cfg5 (12..24)")
     ap.add_argument("--impl", default="dvqls", choices=["dvqls", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    w = CONFIGS[args.config]()
+    w = CONFIGS[args.config](args.n) if args.config == "cfg5" else CONFIGS[args.config]()
 
     if args.impl == "reference":
         return run_reference(args, w)
@@ -379,7 +398,7 @@ def main():
             },
             "evals_per_s": KT * args.steps / (dev_ms * 1e-3),
             "kernel_ms": {"prefix": pre_ms, "hadamard": had_ms, "reduce": red_ms},
-            "roofline": {
+            "roofline": streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src) if w.n > 12 else {
                 "bound": "alu",
                 "kernel": "hadamard_kernel",
                 "achieved": achieved_ops / 1e12,

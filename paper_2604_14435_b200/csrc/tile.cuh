@@ -160,12 +160,33 @@ tile_hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restr
         const bool zhere = pass == ng - 1; // Z_j between the two transforms
         const uint32_t ntiles = N >> geo.tb;
         for (uint32_t tile = 0; tile < ntiles; ++tile) {
-          // ---- load ----
+          // ---- load: cp.async global -> SMEM, all copies of the tile in flight at once ----
+          // (pass 0 copies the UNSIGNED x[j ^ m_k]; the Pauli sign of c-A_k is applied in
+          //  the first SMEM round below)
           for (int e = t; e < (1 << geo.tb); e += THREADS) {
             const uint32_t j = geo.gidx(tile, e);
-            s[tslot(e)] = first ? sgather(x, j, Tk.xm, Tk.zm) : phi[j];
+            const double2* src = first ? (x + (j ^ Tk.xm)) : (phi + j);
+            const uint32_t dst = uint32_t(__cvta_generic_to_shared(s + tslot(e)));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
           }
+          asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
           __syncthreads();
+          if (first && !HH) {  // sgn_k(j ^ m_k) = (-1)^{popcount((j ^ m_k) & z_k)}
+            for (int e = t; e < (1 << geo.tb); e += THREADS)
+              if (__popc((geo.gidx(tile, e) ^ Tk.xm) & Tk.zm) & 1) {
+                const double2 f = s[tslot(e)];
+                s[tslot(e)] = make_double2(-f.x, -f.y);
+              }
+            __syncthreads();
+          }
+          if (first && HH) {
+            for (int e = t; e < (1 << geo.tb); e += THREADS)
+              if (__popc((geo.gidx(tile, e) ^ Tk.xm) & Tk.zm) & 1) {
+                const double2 f = s[tslot(e)];
+                s[tslot(e)] = make_double2(-f.x, -f.y);
+              }
+            __syncthreads();
+          }
           // ---- FWHT rounds on tile bits [c, tb) ----
           const int nr = TBITS / RB;
           if (HH) {
@@ -239,7 +260,7 @@ tile_hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restr
               acc += (q & 1) ? (xl.x * f.y - xl.y * f.x) : (xl.x * f.x + xl.y * f.y);
             }
           } else {
-            for (int e = t; e < (1 << geo.tb); e += THREADS) phi[geo.gidx(tile, e)] = s[tslot(e)];
+            for (int e = t; e < (1 << geo.tb); e += THREADS) __stcs(phi + geo.gidx(tile, e), s[tslot(e)]);
           }
           __syncthreads();
         }
