@@ -242,7 +242,9 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
-    ap.add_argument("--batch", type=int, default=1, help="thetas per step (dvqls_cost_dev K)")
+    ap.add_argument("--batch", type=int, default=16,
+                    help="thetas per step (dvqls_cost_dev K): one batch of FD-gradient points, the way the "
+                         "config-2 L-BFGS-B loop calls the path; K=1 is measured and reported beside it")
     ap.add_argument("--n", type=int, default=16, help="qubits for --config cfg5 (12..24)")
     ap.add_argument("--impl", default="dvqls", choices=["dvqls", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -334,6 +336,26 @@ def main():
         sampler.__exit__()
     dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     dev_ms = max_over_ranks(dev_ms)
+
+    # ---- the same timed loop with a single theta per step (K = 1) -------------------------------
+    k1_steps = max(3, args.steps // 2)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.zero_()
+            ctx.cost_dev(1, th_dev, out_dev)
+        barrier()
+        s1 = [torch.cuda.Event(enable_timing=True) for _ in range(k1_steps)]
+        e1 = [torch.cuda.Event(enable_timing=True) for _ in range(k1_steps)]
+        k1t = []
+        for i in range(k1_steps):
+            flush.zero_()
+            s1[i].record(stream)
+            ctx.cost_dev(1, th_dev, out_dev)
+            e1[i].record(stream)
+            k1t.append(ctx.last_timings())
+        barrier()
+    k1_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in zip(s1, e1)))
+    res1 = out_dev[:5].cpu().numpy()
     res = out_dev.view(KT, 5).cpu().numpy()
     if not np.all(np.isfinite(res[:, 0])):
         print("error: non-finite cost", res, file=sys.stderr)
@@ -397,6 +419,12 @@ def main():
                 "parallelism": f"dp{world} (contiguous circuit blocks, one NCCL allreduce of 4 fp64 per theta)",
             },
             "evals_per_s": KT * args.steps / (dev_ms * 1e-3),
+            "k1": {"value": w.n_circuits * k1_steps / (k1_ms * 1e-3), "unit": "circuits/s",
+                   "ms_per_step": k1_ms / k1_steps, "evals_per_s": k1_steps / (k1_ms * 1e-3),
+                   "kernel_ms": {"prefix": statistics.mean(t["prefix_ms"] for t in k1t),
+                                 "hadamard": statistics.mean(t["hadamard_ms"] for t in k1t),
+                                 "reduce": statistics.mean(t["reduce_ms"] for t in k1t)},
+                   "note": "one cost evaluation per step (same loop, same L2 flush)"},
             "kernel_ms": {"prefix": pre_ms, "hadamard": had_ms, "reduce": red_ms},
             "roofline": streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src) if w.n > 12 else {
                 "bound": "alu",
@@ -420,6 +448,7 @@ def main():
             "gpu_launches": args.steps * ctx.launches_per_call(),
             "clocks": clocks,
             "cost": float(res[0, 0]),
+            "cost_k1": float(res1[0]),
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(w, thetas[0])

@@ -117,6 +117,7 @@ struct dvqls_ctx {
   double* d_out = nullptr;       // max_batch * 5
   double* d_gather = nullptr;    // world * chunk (terms allgather)
   double* h_stage = nullptr;     // pinned staging
+  unsigned* d_counter = nullptr; // last-CTA tickets, one per theta slot
   bool tile_path = false;        // n > 10
   double2* d_scratch = nullptr;  // grid * N (n > 12)
   double2* d_x2 = nullptr;       // ring ping-pong buffer (n > 12 prefix)
@@ -161,17 +162,22 @@ int fail(dvqls_ctx* c, int code, const char* fmt, ...) {
 thread_local std::string g_create_err;
 
 // Hadamard-test kernel over circuits [c0, c0 + C) (or the list cidx[0..C)) of every theta.
-int launch_hadamard(dvqls_ctx* ctx, int K, int64_t c0, int64_t C, const int64_t* cidx, double* terms, int grid) {
+// red_out != NULL: the kernel's last CTA per theta also performs the fixed-order reduction
+// (with_cost: 5 doubles C, E, Psi per theta; else 4 doubles E, Psi for the allreduce).
+int launch_hadamard(dvqls_ctx* ctx, int K, int64_t c0, int64_t C, const int64_t* cidx, double* terms, int grid,
+                    double* red_out = nullptr, int with_cost = 0) {
   dim3 g(grid, K);
   if (!ctx->tile_path) {
     void* args[] = {(void*)&ctx->d_x,   (void*)&ctx->d_tab, (void*)&ctx->d_coef,  (void*)&ctx->d_hv,
                     (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&c0, (void*)&C,
-                    (void*)&terms, (void*)&ctx->d_partials};
+                    (void*)&terms, (void*)&ctx->d_partials, (void*)&with_cost, (void*)&red_out,
+                    (void*)&ctx->d_counter};
     CK(cudaLaunchKernel(ctx->kc.fn, g, dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
   } else {
     void* args[] = {(void*)&ctx->d_x, (void*)&ctx->d_tab, (void*)&ctx->d_coef, (void*)&ctx->d_hv,
                     (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&ctx->n, (void*)&c0, (void*)&C,
-                    (void*)&cidx, (void*)&ctx->d_scratch, (void*)&terms, (void*)&ctx->d_partials};
+                    (void*)&cidx, (void*)&ctx->d_scratch, (void*)&terms, (void*)&ctx->d_partials,
+                    (void*)&with_cost, (void*)&red_out, (void*)&ctx->d_counter};
     CK(cudaLaunchKernel(ctx->kc.fn, g, dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
   }
   return DVQLS_OK;
@@ -216,17 +222,14 @@ int launch_eval(dvqls_ctx* ctx, int K, const double* thetas_dev, bool want_cost,
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], ctx->stream));
   const int64_t Cloc = ctx->c1 - ctx->c0;
   {
-    int rc = launch_hadamard(ctx, K, ctx->c0, Cloc, nullptr, ctx->d_terms, ctx->grid);
+    // a9 (+ a10 on one rank) fused into the kernel tail (last-CTA fixed-order reduction)
+    double* red = want_cost ? (ctx->world == 1 ? out_dev : ctx->d_ep) : nullptr;
+    int rc = launch_hadamard(ctx, K, ctx->c0, Cloc, nullptr, ctx->d_terms, ctx->grid, red, ctx->world == 1 ? 1 : 0);
     if (rc) return rc;
   }
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
   if (want_cost) {
-    if (ctx->world == 1) {
-      reduce_kernel<<<K, REDUCE_THREADS, 0, ctx->stream>>>(ctx->d_partials, ctx->NG, ctx->n, 1, out_dev);
-      CK(cudaGetLastError());
-    } else {
-      reduce_kernel<<<K, REDUCE_THREADS, 0, ctx->stream>>>(ctx->d_partials, ctx->NG, ctx->n, 0, ctx->d_ep);
-      CK(cudaGetLastError());
+    if (ctx->world > 1) {
       CKN(nccl().AllReduce(ctx->d_ep, ctx->d_ep, size_t(4) * K, ncclDouble, ncclSum, ctx->comm, ctx->stream));
       finalize_kernel<<<1, 32 * ((K + 31) / 32), 0, ctx->stream>>>(ctx->d_ep, K, ctx->n, out_dev);
       CK(cudaGetLastError());
@@ -244,7 +247,7 @@ void release(dvqls_ctx* c) {
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
   cudaFree(c->d_tab); cudaFree(c->d_coef); cudaFree(c->d_hv); cudaFree(c->d_theta); cudaFree(c->d_x);
   cudaFree(c->d_terms); cudaFree(c->d_partials); cudaFree(c->d_ep); cudaFree(c->d_out); cudaFree(c->d_gather);
-  cudaFree(c->d_scratch); cudaFree(c->d_x2); cudaFree(c->d_gates); cudaFree(c->d_cidx); cudaFree(c->d_sub);
+  cudaFree(c->d_counter); cudaFree(c->d_scratch); cudaFree(c->d_x2); cudaFree(c->d_gates); cudaFree(c->d_cidx); cudaFree(c->d_sub);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -431,6 +434,13 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
       fail(ctx, DVQLS_E_CUDA, "prefix_gate_pass smem");
       return bail(DVQLS_E_CUDA);
     }
+  } else if (ctx->prefix_rb == 0 && n >= 7) {  // 4 amplitudes per thread, shuffles + 2 transposes/layer
+    static const void* quads[11] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                    (const void*)&prefix_quad_kernel<7>, (const void*)&prefix_quad_kernel<8>,
+                                    (const void*)&prefix_quad_kernel<9>, (const void*)&prefix_quad_kernel<10>};
+    ctx->prefix_fn = quads[n];
+    ctx->prefix_threads = std::max(32, ctx->N / 4);
+    ctx->prefix_smem = sizeof(double2) * (size_t(ctx->N) + 2 * size_t(n) * layers) + sizeof(int) * ctx->N;
   } else if (ctx->prefix_rb == 0) {  // one amplitude per thread, shuffles + 2 transposes per layer
     static const void* lanes[11] = {nullptr,
                                     (const void*)&prefix_lanes_kernel<1>, (const void*)&prefix_lanes_kernel<2>,
@@ -465,6 +475,7 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
       alloc((void**)&ctx->d_partials, sizeof(double) * KB * ctx->NG * 4) ||
       alloc((void**)&ctx->d_ep, sizeof(double) * KB * 4) || alloc((void**)&ctx->d_out, sizeof(double) * KB * 5) ||
       (ctx->world > 1 && alloc((void**)&ctx->d_gather, sizeof(double) * ctx->world * ctx->chunk)) ||
+      alloc((void**)&ctx->d_counter, sizeof(unsigned) * KB) ||
       (n > 12 && alloc((void**)&ctx->d_scratch, sizeof(double2) * size_t(ctx->grid) * ctx->N)) ||
       (n > 12 && alloc((void**)&ctx->d_x2, sizeof(double2) * size_t(ctx->N))) ||
       (n > 12 && alloc((void**)&ctx->d_gates, sizeof(double2) * 2 * size_t(n) * layers))) {
@@ -476,7 +487,8 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
     fail(ctx, DVQLS_E_CUDA, "cudaMallocHost failed");
     return bail(DVQLS_E_CUDA);
   }
-  if (cudaMemcpy(ctx->d_tab, tab.data(), sizeof(PauliTerm) * L, cudaMemcpyHostToDevice) ||
+  if (cudaMemset(ctx->d_counter, 0, sizeof(unsigned) * KB) ||
+      cudaMemcpy(ctx->d_tab, tab.data(), sizeof(PauliTerm) * L, cudaMemcpyHostToDevice) ||
       cudaMemcpy(ctx->d_coef, coef.data(), sizeof(double2) * L, cudaMemcpyHostToDevice) ||
       (!hv.empty() && cudaMemcpy(ctx->d_hv, hv.data(), sizeof(double2) * ctx->N, cudaMemcpyHostToDevice))) {
     fail(ctx, DVQLS_E_CUDA, "table upload failed");
@@ -663,7 +675,10 @@ void* dvqls_stream(const dvqls_ctx* ctx) { return ctx ? (void*)ctx->stream : nul
 
 int dvqls_launches_per_call(const dvqls_ctx* ctx) {
   if (!ctx) return DVQLS_E_ARG;
-  return ctx->world == 1 ? 3 : 4;  // prefix, hadamard, reduce [, finalize]  (+ NCCL kernel)
+  // prefix (1, or 2 + layers*(groups+1) for the global n > 12 prefix), hadamard (+ fused
+  // reduction) [, finalize]  (+ NCCL's own allreduce kernel when world > 1)
+  const int pre = ctx->prefix_rb < 0 ? 2 + ctx->layers * ((ctx->n <= 21 ? 2 : 3) + 1) : 1;
+  return pre + 1 + (ctx->world == 1 ? 0 : 1);
 }
 
 int dvqls_last_timings(const dvqls_ctx* c, float* ms) {

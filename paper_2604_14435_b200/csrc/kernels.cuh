@@ -278,6 +278,187 @@ prefix_lanes_kernel(int layers, int entangler, const double* __restrict__ thetas
 }
 
 // ---------------------------------------------------------------------------
+// a2 for 7 <= n <= 10: four amplitudes per thread (2^(n-2) threads, <= 8 warps).
+//   layout X: i = (w << 7) | (l << 2) | r     r: 2 register bits, l: 5 lane bits, w: W = n-7 bits
+//   layout Y: warp bits <-> lane bits 0..W-1 swapped: positions 7..n-1 become lane bits 0..W-1
+// Register-bit gates are in-thread 2x2 complex matvecs; lane-bit gates are one shuffle per
+// amplitude + a 2-term complex dot.  The gate coefficients are loaded once per warp and gate
+// and reused for the thread's 4 independent amplitudes (4x fewer SMEM wavefronts per
+// amplitude than one amplitude per thread; measured SMEM-bound otherwise).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int qswz(int i) { return i ^ ((i >> 2) & 7) ^ ((i >> 7) & 7); }
+
+template <int NQ>
+__global__ void __launch_bounds__(256)
+prefix_quad_kernel(int layers, int entangler, const double* __restrict__ thetas, double2* __restrict__ x_all) {
+  constexpr int n = NQ;
+  constexpr int N = 1 << n;
+  constexpr int W = n - 7;
+  extern __shared__ double2 qsm[];
+  const int P = 3 * n * layers;
+  const int G = n * layers;
+  double2* sbuf = qsm;                            // N amplitudes (transposes)
+  double2* tabU = qsm + N;                        // 2 per gate: a, b of U = [[a, -b*], [b, a*]]
+  int* perm = reinterpret_cast<int*>(tabU + 2 * G);
+  const double* th = thetas + (size_t)blockIdx.x * P;
+  const int tid = threadIdx.x;
+  const int l = tid & 31, w = tid >> 5;
+  const unsigned full = 0xffffffffu;
+
+  for (int g = tid; g < G; g += blockDim.x) {
+    double s0, c0, s1, c1, s2, c2;
+    sincos(0.5 * th[3 * g + 0], &s0, &c0);
+    sincos(0.5 * th[3 * g + 1], &s1, &c1);
+    sincos(0.5 * th[3 * g + 2], &s2, &c2);
+    tabU[2 * g + 0] = make_double2(c1 * (c2 * c0 - s2 * s0), -s1 * (c2 * c0 + s2 * s0));
+    tabU[2 * g + 1] = make_double2(c1 * (s2 * c0 + c2 * s0), s1 * (c2 * s0 - s2 * c0));
+  }
+  for (int i = tid; i < N; i += blockDim.x) {
+    int e = i;
+    if (entangler == 0) {
+      int j = i;  // new[i] = old[c_0(c_1(...c_{n-1}(i)))]
+#pragma unroll
+      for (int q = n - 1; q >= 0; --q) {
+        const int pc = n - 1 - q, pt = n - 1 - ((q + 1) % n);
+        if ((j >> pc) & 1) j ^= 1 << pt;
+      }
+      e = j;
+    } else {
+      int par = 0;
+#pragma unroll
+      for (int q = 0; q < n; ++q) par ^= ((i >> (n - 1 - q)) & (i >> (n - 1 - (q + 1) % n))) & 1;
+      e = int(unsigned(i) | (unsigned(par) << 31));
+    }
+    perm[i] = e;
+  }
+  __syncthreads();
+
+  // element indices of this thread's 4 amplitudes in both layouts
+  const int iX0 = (w << 7) | (l << 2);
+  const int iY0 = ((l >> W) << (2 + W)) | (w << 2) | ((l & ((1 << W) - 1)) << 7);
+  int pX[4];
+  bool nX[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int e = perm[iX0 | r];
+    pX[r] = qswz(e & 0x7fffffff);
+    nX[r] = e < 0;
+  }
+  double2 v[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) v[r] = make_double2((iX0 | r) == 0 ? 1.0 : 0.0, 0.0);
+
+  // 2x2 gate on register bit RBIT (positions 0, 1)
+  auto reg_gate = [&](int g, int rbit) {
+    const double2 ua = tabU[2 * g], ub = tabU[2 * g + 1];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (!(r & (1 << rbit))) {
+        const double2 x0 = v[r], x1 = v[r | (1 << rbit)];
+        v[r] = make_double2(fma(ua.x, x0.x, fma(-ua.y, x0.y, fma(-ub.x, x1.x, -ub.y * x1.y))),
+                            fma(ua.x, x0.y, fma(ua.y, x0.x, fma(-ub.x, x1.y, ub.y * x1.x))));
+        v[r | (1 << rbit)] = make_double2(fma(ub.x, x0.x, fma(-ub.y, x0.y, fma(ua.x, x1.x, ua.y * x1.y))),
+                                          fma(ub.x, x0.y, fma(ub.y, x0.x, fma(ua.x, x1.y, -ua.y * x1.x))));
+      }
+  };
+  // gate on lane bit LBIT: row of U selected by the thread's bit; partner amplitude by shuffle
+  auto lane_gate = [&](int g, int lbit) {
+    const double2 ua = tabU[2 * g], ub = tabU[2 * g + 1];
+    const bool bit = (l >> lbit) & 1;
+    // bit 0: self = a, other = -conj(b);  bit 1: self = conj(a), other = b
+    const double2 cs = make_double2(ua.x, bit ? -ua.y : ua.y);
+    const double2 co = make_double2(bit ? ub.x : -ub.x, ub.y);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const double2 pp =
+          make_double2(__shfl_xor_sync(full, v[r].x, 1 << lbit), __shfl_xor_sync(full, v[r].y, 1 << lbit));
+      const double sr = fma(cs.x, v[r].x, -cs.y * v[r].y), si = fma(cs.x, v[r].y, cs.y * v[r].x);
+      v[r] = make_double2(sr + fma(co.x, pp.x, -co.y * pp.y), si + fma(co.x, pp.y, co.y * pp.x));
+    }
+  };
+
+  for (int layer = 0; layer < layers; ++layer) {
+    const int gl = layer * n;  // gate of qubit q is gl + q, qubit q <-> position n - 1 - q
+    reg_gate(gl + (n - 1 - 0), 0);
+    reg_gate(gl + (n - 1 - 1), 1);
+#pragma unroll
+    for (int pos = 2; pos < 7; ++pos) lane_gate(gl + (n - 1 - pos), pos - 2);
+    if (W > 0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) sbuf[qswz(iX0 | r)] = v[r];
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 4; ++r) v[r] = sbuf[qswz(iY0 | r)];
+      __syncthreads();
+#pragma unroll
+      for (int pos = 7; pos < n; ++pos) lane_gate(gl + (n - 1 - pos), pos - 7);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) sbuf[qswz(iY0 | r)] = v[r];
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) sbuf[qswz(iX0 | r)] = v[r];
+    }
+    __syncthreads();
+    // entangling ring folded into the read back to layout X
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const double2 a = sbuf[pX[r]];
+      v[r] = nX[r] ? make_double2(-a.x, -a.y) : a;
+    }
+    __syncthreads();
+  }
+  double2* x = x_all + (size_t)blockIdx.x * N;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) x[iX0 | r] = v[r];
+}
+
+// ---------------------------------------------------------------------------
+// a9/a10 fused into the Hadamard kernels: the last CTA of a theta to finish (ticket
+// counter) sums the NG partial quadruples in a fixed order and writes (C, E, Psi) or
+// (E, Psi) for the cross-rank allreduce.  Bitwise identical to reduce_kernel's order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double cost_of_dev(double ReE, double RePsi, int n) {
+  return RePsi <= 1e-12 ? __longlong_as_double(0x7ff8000000000000ll) : 0.5 - 0.5 * ReE / (double(n) * RePsi);
+}
+
+__device__ void finish_partials(const double* __restrict__ partials, int64_t NG, int kth, int n, int with_cost,
+                                double* __restrict__ out, unsigned* __restrict__ counter) {
+  __shared__ unsigned s_last;
+  __shared__ double sred[4][32];
+  __threadfence();  // partials of this CTA visible device-wide before the ticket
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(counter + kth, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const double* p = partials + (size_t)kth * NG * 4;
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  for (int64_t i = threadIdx.x; i < NG; i += blockDim.x) {
+    a0 += __ldcg(p + 4 * i + 0); a1 += __ldcg(p + 4 * i + 1);
+    a2 += __ldcg(p + 4 * i + 2); a3 += __ldcg(p + 4 * i + 3);
+  }
+  for (int off = 16; off >= 1; off >>= 1) {
+    a0 += __shfl_xor_sync(0xffffffffu, a0, off); a1 += __shfl_xor_sync(0xffffffffu, a1, off);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, off); a3 += __shfl_xor_sync(0xffffffffu, a3, off);
+  }
+  const int wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if ((threadIdx.x & 31) == 0) { sred[0][wid] = a0; sred[1][wid] = a1; sred[2][wid] = a2; sred[3][wid] = a3; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double e0 = 0, e1 = 0, e2 = 0, e3 = 0;
+    for (int w = 0; w < nw; ++w) { e0 += sred[0][w]; e1 += sred[1][w]; e2 += sred[2][w]; e3 += sred[3][w]; }
+    if (with_cost) {
+      double* o = out + (size_t)kth * 5;
+      o[0] = cost_of_dev(e0, e2, n); o[1] = e0; o[2] = e1; o[3] = e2; o[4] = e3;
+    } else {
+      double* o = out + (size_t)kth * 4;
+      o[0] = e0; o[1] = e1; o[2] = e2; o[3] = e3;
+    }
+    counter[kth] = 0u;  // ready for the next call (stream-ordered)
+  }
+}
+
+// ---------------------------------------------------------------------------
 // a3-a9: batched Hadamard-test kernel for n = NQ system qubits.
 //
 // A circuit is owned by a group of GT = 2^TB threads, each holding R = 2^RB
@@ -482,7 +663,8 @@ template <int NQ, int WARPS, bool HH>
 __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(reg_cap<WARPS>())
 hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ tab,
                 const double2* __restrict__ coef, const double2* __restrict__ hv, double hv_scale, int L,
-                int64_t c0, int64_t C, double* __restrict__ out_terms, double* __restrict__ partials) {
+                int64_t c0, int64_t C, double* __restrict__ out_terms, double* __restrict__ partials,
+                int with_cost, double* __restrict__ red_out, unsigned* __restrict__ counter) {
   using S = Shape<NQ>;
   constexpr int TB = S::TB, RB = S::RB, GT = S::GT, R = S::R, N = S::N, GPW = S::GPW;
   double2* smem = dvqls_smem;
@@ -595,6 +777,7 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
     double* o = partials + ((size_t)kth * NG + g) * 4;
     o[0] = acc4[0]; o[1] = acc4[1]; o[2] = acc4[2]; o[3] = acc4[3];
   }
+  if (red_out) finish_partials(partials, NG, kth, NQ, with_cost, red_out, counter);
 }
 
 // ---------------------------------------------------------------------------

@@ -143,6 +143,47 @@ __global__ void __launch_bounds__(THREADS) k_mixed(double b, int iters_d, int it
   out[blockIdx.x * THREADS + threadIdx.x] = r;
 }
 
+// dependent-chain latencies (one warp): cycles per dependent op
+__global__ void k_lat_dfma(double b, int iters, double* out, long long* cyc) {
+  double a = threadIdx.x;
+  const double m = 1.0 + b;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) { a = fma(a, m, b); a = fma(a, m, b); a = fma(a, m, b); a = fma(a, m, b); }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[threadIdx.x] = a;
+}
+__global__ void k_lat_dadd(double b, int iters, double* out, long long* cyc) {
+  double a = threadIdx.x;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) { a = a + b; a = a + b; a = a + b; a = a + b; }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[threadIdx.x] = a;
+}
+__global__ void k_lat_shfl(int iters, unsigned* out, long long* cyc) {
+  unsigned a = threadIdx.x;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    a = __shfl_xor_sync(0xffffffffu, a, 1); a = __shfl_xor_sync(0xffffffffu, a, 2);
+    a = __shfl_xor_sync(0xffffffffu, a, 4); a = __shfl_xor_sync(0xffffffffu, a, 8);
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[threadIdx.x] = a;
+}
+__global__ void k_lat_lds(int iters, unsigned* out, long long* cyc) {
+  __shared__ unsigned s[1024];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) s[i] = (i * 7 + 1) & 1023;
+  __syncthreads();
+  unsigned a = threadIdx.x;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) { a = s[a]; a = s[a]; a = s[a]; a = s[a]; }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[threadIdx.x] = a;
+}
+
 int main() {
   cudaDeviceProp p;
   CK(cudaGetDeviceProperties(&p, 0));
@@ -182,6 +223,19 @@ int main() {
   c = med();
   const double t_d = (THREADS / 2.0) * itd * 8 / 64.0, t_l = (THREADS / 2.0) * itl * 8 * 16 / 128.0;
   printf(", \"mixed_cycles\": %.0f, \"mixed_model_sum\": %.0f, \"mixed_model_max\": %.0f", c, t_d + t_l, std::max(t_d, t_l));
+  {
+    const int li = 1024;
+    k_lat_dfma<<<1, 32>>>(1e-9, li, dout, dcyc); CK(cudaDeviceSynchronize());
+    long long c1; CK(cudaMemcpy(&c1, dcyc, 8, cudaMemcpyDeviceToHost));
+    k_lat_dadd<<<1, 32>>>(1e-9, li, dout, dcyc); CK(cudaDeviceSynchronize());
+    long long c2; CK(cudaMemcpy(&c2, dcyc, 8, cudaMemcpyDeviceToHost));
+    k_lat_shfl<<<1, 32>>>(li, uout, dcyc); CK(cudaDeviceSynchronize());
+    long long c3; CK(cudaMemcpy(&c3, dcyc, 8, cudaMemcpyDeviceToHost));
+    k_lat_lds<<<1, 32>>>(li, uout, dcyc); CK(cudaDeviceSynchronize());
+    long long c4; CK(cudaMemcpy(&c4, dcyc, 8, cudaMemcpyDeviceToHost));
+    printf(", \"dfma_latency_clk\": %.1f, \"dadd_latency_clk\": %.1f, \"shfl_latency_clk\": %.1f, \"lds32_latency_clk\": %.1f",
+           double(c1) / (4 * li), double(c2) / (4 * li), double(c3) / (4 * li), double(c4) / (4 * li));
+  }
   printf("}\n");
   return 0;
 }
