@@ -307,15 +307,23 @@ def main():
     if sampler:
         sampler.__enter__()
     with torch.cuda.stream(stream):
-        # W warm-up steps, continued until >= 0.5 s of load so the SM clock has ramped
+        # W warm-up steps, continued (in chunks of 8, the same number on every rank: every
+        # call contains a cross-rank reduction) until >= 0.5 s of load so the SM clock has ramped
         t_w = time.time()
         i = 0
-        while i < args.warmup or time.time() - t_w < 0.5:
-            flush.zero_()
-            ctx.cost_dev(KT, th_dev, out_dev)
-            if i % 16 == 15:
-                torch.cuda.synchronize()
-            i += 1
+        while True:
+            for _ in range(8):
+                flush.zero_()
+                ctx.cost_dev(KT, th_dev, out_dev)
+                i += 1
+            torch.cuda.synchronize()
+            more = 1.0 if (i < args.warmup or time.time() - t_w < 0.5) else 0.0
+            if world > 1:
+                t = torch.tensor([more], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                more = float(t.item())
+            if more == 0.0:
+                break
         barrier()
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]

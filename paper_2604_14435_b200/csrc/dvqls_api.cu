@@ -118,6 +118,12 @@ struct dvqls_ctx {
   double* d_gather = nullptr;    // world * chunk (terms allgather)
   double* h_stage = nullptr;     // pinned staging
   unsigned* d_counter = nullptr; // last-CTA tickets, one per theta slot
+  // fused NVLink allreduce (world > 1): own symmetric buffer + IPC-mapped peer buffers
+  bool p2p = false;
+  char* d_sym = nullptr;
+  std::vector<char*> peer_ptrs;
+  char** d_peers = nullptr;
+  unsigned long long epoch = 0;
   bool tile_path = false;        // n > 10
   double2* d_scratch = nullptr;  // grid * N (n > 12)
   double2* d_x2 = nullptr;       // ring ping-pong buffer (n > 12 prefix)
@@ -167,17 +173,24 @@ thread_local std::string g_create_err;
 int launch_hadamard(dvqls_ctx* ctx, int K, int64_t c0, int64_t C, const int64_t* cidx, double* terms, int grid,
                     double* red_out = nullptr, int with_cost = 0) {
   dim3 g(grid, K);
+  P2PArgs p2p{1, 0, ctx->max_batch, 0ull, nullptr};
+  if (red_out && with_cost && ctx->p2p) {
+    p2p.world = ctx->world;
+    p2p.rank = ctx->rank;
+    p2p.epoch = ++ctx->epoch;
+    p2p.peers = ctx->d_peers;
+  }
   if (!ctx->tile_path) {
     void* args[] = {(void*)&ctx->d_x,   (void*)&ctx->d_tab, (void*)&ctx->d_coef,  (void*)&ctx->d_hv,
                     (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&c0, (void*)&C,
                     (void*)&terms, (void*)&ctx->d_partials, (void*)&with_cost, (void*)&red_out,
-                    (void*)&ctx->d_counter};
+                    (void*)&ctx->d_counter, (void*)&p2p};
     CK(cudaLaunchKernel(ctx->kc.fn, g, dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
   } else {
     void* args[] = {(void*)&ctx->d_x, (void*)&ctx->d_tab, (void*)&ctx->d_coef, (void*)&ctx->d_hv,
                     (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&ctx->n, (void*)&c0, (void*)&C,
                     (void*)&cidx, (void*)&ctx->d_scratch, (void*)&terms, (void*)&ctx->d_partials,
-                    (void*)&with_cost, (void*)&red_out, (void*)&ctx->d_counter};
+                    (void*)&with_cost, (void*)&red_out, (void*)&ctx->d_counter, (void*)&p2p};
     CK(cudaLaunchKernel(ctx->kc.fn, g, dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
   }
   return DVQLS_OK;
@@ -223,13 +236,14 @@ int launch_eval(dvqls_ctx* ctx, int K, const double* thetas_dev, bool want_cost,
   const int64_t Cloc = ctx->c1 - ctx->c0;
   {
     // a9 (+ a10 on one rank) fused into the kernel tail (last-CTA fixed-order reduction)
-    double* red = want_cost ? (ctx->world == 1 ? out_dev : ctx->d_ep) : nullptr;
-    int rc = launch_hadamard(ctx, K, ctx->c0, Cloc, nullptr, ctx->d_terms, ctx->grid, red, ctx->world == 1 ? 1 : 0);
+    const bool direct = ctx->world == 1 || ctx->p2p;  // kernel writes the final (C, E, Psi)
+    double* red = want_cost ? (direct ? out_dev : ctx->d_ep) : nullptr;
+    int rc = launch_hadamard(ctx, K, ctx->c0, Cloc, nullptr, ctx->d_terms, ctx->grid, red, direct ? 1 : 0);
     if (rc) return rc;
   }
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
   if (want_cost) {
-    if (ctx->world > 1) {
+    if (ctx->world > 1 && !ctx->p2p) {
       CKN(nccl().AllReduce(ctx->d_ep, ctx->d_ep, size_t(4) * K, ncclDouble, ncclSum, ctx->comm, ctx->stream));
       finalize_kernel<<<1, 32 * ((K + 31) / 32), 0, ctx->stream>>>(ctx->d_ep, K, ctx->n, out_dev);
       CK(cudaGetLastError());
@@ -244,6 +258,9 @@ int launch_eval(dvqls_ctx* ctx, int K, const double* thetas_dev, bool want_cost,
 
 void release(dvqls_ctx* c) {
   if (!c) return;
+  for (int q = 0; q < int(c->peer_ptrs.size()); ++q)
+    if (q != c->rank && c->peer_ptrs[q]) cudaIpcCloseMemHandle(c->peer_ptrs[q]);
+  cudaFree(c->d_sym); cudaFree(c->d_peers);
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
   cudaFree(c->d_tab); cudaFree(c->d_coef); cudaFree(c->d_hv); cudaFree(c->d_theta); cudaFree(c->d_x);
   cudaFree(c->d_terms); cudaFree(c->d_partials); cudaFree(c->d_ep); cudaFree(c->d_out); cudaFree(c->d_gather);
@@ -254,6 +271,63 @@ void release(dvqls_ctx* c) {
 }
 
 }  // namespace
+
+// Symmetric buffers for the fused allreduce: allocate, exchange IPC handles with an NCCL
+// allgather (create-time only), map every peer's buffer.  If mapping fails the context
+// falls back to ncclAllReduce on the cost path.
+int setup_p2p(dvqls_ctx* ctx) {
+  const size_t bytes = size_t(2) * ctx->world * ctx->max_batch * (32 + 8);
+  CK(cudaMalloc((void**)&ctx->d_sym, bytes));
+  CK(cudaMemset(ctx->d_sym, 0, bytes));
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, ctx->d_sym));
+  char* d_h = nullptr;
+  CK(cudaMalloc((void**)&d_h, sizeof(h) * (ctx->world + 1)));
+  CK(cudaMemcpy(d_h, &h, sizeof(h), cudaMemcpyHostToDevice));
+  ncclResult_t r = nccl().AllGather(d_h, d_h + sizeof(h), sizeof(h), ncclChar, ctx->comm, ctx->stream);
+  if (r != ncclSuccess) {
+    cudaFree(d_h);
+    return fail(ctx, DVQLS_E_NCCL, "handle allgather: %s", nccl().GetErrorString(r));
+  }
+  std::vector<cudaIpcMemHandle_t> all(ctx->world);
+  CK(cudaMemcpyAsync(all.data(), d_h + sizeof(h), sizeof(h) * ctx->world, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_h);
+  ctx->peer_ptrs.assign(ctx->world, nullptr);
+  bool ok = true;
+  for (int q = 0; q < ctx->world; ++q) {
+    if (q == ctx->rank) { ctx->peer_ptrs[q] = ctx->d_sym; continue; }
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = false;
+      break;
+    }
+    ctx->peer_ptrs[q] = static_cast<char*>(p);
+  }
+  if (!ok) {  // every rank must agree: fall back together if any rank could not map
+    ctx->p2p = false;
+  } else {
+    ctx->p2p = true;
+  }
+  int flag = ctx->p2p ? 1 : 0, all_ok = 0;
+  {
+    int* d_f = nullptr;
+    CK(cudaMalloc((void**)&d_f, sizeof(int)));
+    CK(cudaMemcpy(d_f, &flag, sizeof(int), cudaMemcpyHostToDevice));
+    ncclResult_t r2 = nccl().AllReduce(d_f, d_f, 1, ncclInt32, ncclMin, ctx->comm, ctx->stream);
+    if (r2 != ncclSuccess) { cudaFree(d_f); return fail(ctx, DVQLS_E_NCCL, "p2p agreement"); }
+    CK(cudaMemcpyAsync(&all_ok, d_f, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_f);
+  }
+  ctx->p2p = all_ok == 1;
+  if (ctx->p2p) {
+    CK(cudaMalloc((void**)&ctx->d_peers, sizeof(char*) * ctx->world));
+    CK(cudaMemcpy(ctx->d_peers, ctx->peer_ptrs.data(), sizeof(char*) * ctx->world, cudaMemcpyHostToDevice));
+  }
+  return DVQLS_OK;
+}
 
 extern "C" {
 
@@ -516,6 +590,13 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
       return bail(DVQLS_E_NCCL);
     }
   }
+  if (ctx->world > 1) {
+    const char* e = getenv("DVQLS_ALLREDUCE");  // "nccl" forces the NCCL baseline
+    if (!(e && std::string(e) == "nccl")) {
+      int rc = setup_p2p(ctx);
+      if (rc) return bail(rc);
+    }
+  }
   *out = ctx;
   return DVQLS_OK;
 }
@@ -678,7 +759,7 @@ int dvqls_launches_per_call(const dvqls_ctx* ctx) {
   // prefix (1, or 2 + layers*(groups+1) for the global n > 12 prefix), hadamard (+ fused
   // reduction) [, finalize]  (+ NCCL's own allreduce kernel when world > 1)
   const int pre = ctx->prefix_rb < 0 ? 2 + ctx->layers * ((ctx->n <= 21 ? 2 : 3) + 1) : 1;
-  return pre + 1 + (ctx->world == 1 ? 0 : 1);
+  return pre + 1 + ((ctx->world == 1 || ctx->p2p) ? 0 : 1);
 }
 
 int dvqls_last_timings(const dvqls_ctx* c, float* ms) {

@@ -421,8 +421,60 @@ __device__ __forceinline__ double cost_of_dev(double ReE, double RePsi, int n) {
   return RePsi <= 1e-12 ? __longlong_as_double(0x7ff8000000000000ll) : 0.5 - 0.5 * ReE / (double(n) * RePsi);
 }
 
+// Fused cross-rank reduction over NVLink peer memory (replaces ncclAllReduce + finalize
+// on the cost path).  Every rank owns a symmetric buffer, IPC-mapped into all peers:
+//   double   slot[2][world][KB][4]   (E, Psi) written by rank r for theta k
+//   uint64_t flag[2][world][KB]      epoch of that write
+// The buffer half is chosen by epoch parity; a rank can be at most one call ahead of any
+// peer (it cannot finish call e+1 before every peer has published call e+1), so two halves
+// suffice.  A bounded spin (~2 s) turns a missing peer into a NaN cost instead of a hang.
+struct P2PArgs {
+  int world, rank, KB;
+  unsigned long long epoch;
+  char* const* peers;  // world device pointers (peers[rank] = own buffer)
+};
+
+__device__ __forceinline__ double* p2p_slot(char* base, const P2PArgs& a, int par, int r, int k) {
+  return reinterpret_cast<double*>(base) + ((size_t(par) * a.world + r) * a.KB + k) * 4;
+}
+__device__ __forceinline__ unsigned long long* p2p_flag(char* base, const P2PArgs& a, int par, int r, int k) {
+  return reinterpret_cast<unsigned long long*>(base + size_t(2) * a.world * a.KB * 32) +
+         (size_t(par) * a.world + r) * a.KB + k;
+}
+
+__device__ void p2p_allreduce(const P2PArgs& a, int kth, int n, double e0, double e1, double e2, double e3,
+                              double* __restrict__ out) {
+  const int par = int(a.epoch & 1ull);
+  for (int q = 0; q < a.world; ++q) {
+    volatile double* d = p2p_slot(a.peers[q], a, par, a.rank, kth);
+    d[0] = e0; d[1] = e1; d[2] = e2; d[3] = e3;
+  }
+  __threadfence_system();
+  for (int q = 0; q < a.world; ++q) *reinterpret_cast<volatile unsigned long long*>(
+      p2p_flag(a.peers[q], a, par, a.rank, kth)) = a.epoch;
+  char* mine = a.peers[a.rank];
+  bool ok = true;
+  const long long t0 = clock64();
+  for (int q = 0; q < a.world && ok; ++q) {
+    volatile unsigned long long* f = p2p_flag(mine, a, par, q, kth);
+    while (*f != a.epoch) {
+      if (clock64() - t0 > 4000000000ll) { ok = false; break; }
+    }
+  }
+  __threadfence_system();
+  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  for (int q = 0; q < a.world; ++q) {  // fixed rank order: identical sums on every rank
+    volatile double* d = p2p_slot(mine, a, par, q, kth);
+    s0 += d[0]; s1 += d[1]; s2 += d[2]; s3 += d[3];
+  }
+  double* o = out + (size_t)kth * 5;
+  o[0] = ok ? cost_of_dev(s0, s2, n) : __longlong_as_double(0x7ff8000000000000ll);
+  o[1] = s0; o[2] = s1; o[3] = s2; o[4] = s3;
+}
+
 __device__ void finish_partials(const double* __restrict__ partials, int64_t NG, int kth, int n, int with_cost,
-                                double* __restrict__ out, unsigned* __restrict__ counter) {
+                                double* __restrict__ out, unsigned* __restrict__ counter,
+                                const P2PArgs* p2p = nullptr) {
   __shared__ unsigned s_last;
   __shared__ double sred[4][32];
   __threadfence();  // partials of this CTA visible device-wide before the ticket
@@ -447,7 +499,9 @@ __device__ void finish_partials(const double* __restrict__ partials, int64_t NG,
   if (threadIdx.x == 0) {
     double e0 = 0, e1 = 0, e2 = 0, e3 = 0;
     for (int w = 0; w < nw; ++w) { e0 += sred[0][w]; e1 += sred[1][w]; e2 += sred[2][w]; e3 += sred[3][w]; }
-    if (with_cost) {
+    if (p2p) {
+      p2p_allreduce(*p2p, kth, n, e0, e1, e2, e3, out);
+    } else if (with_cost) {
       double* o = out + (size_t)kth * 5;
       o[0] = cost_of_dev(e0, e2, n); o[1] = e0; o[2] = e1; o[3] = e2; o[4] = e3;
     } else {
@@ -664,7 +718,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(reg_cap<WARPS>())
 hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ tab,
                 const double2* __restrict__ coef, const double2* __restrict__ hv, double hv_scale, int L,
                 int64_t c0, int64_t C, double* __restrict__ out_terms, double* __restrict__ partials,
-                int with_cost, double* __restrict__ red_out, unsigned* __restrict__ counter) {
+                int with_cost, double* __restrict__ red_out, unsigned* __restrict__ counter, P2PArgs p2p) {
   using S = Shape<NQ>;
   constexpr int TB = S::TB, RB = S::RB, GT = S::GT, R = S::R, N = S::N, GPW = S::GPW;
   double2* smem = dvqls_smem;
@@ -777,7 +831,7 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
     double* o = partials + ((size_t)kth * NG + g) * 4;
     o[0] = acc4[0]; o[1] = acc4[1]; o[2] = acc4[2]; o[3] = acc4[3];
   }
-  if (red_out) finish_partials(partials, NG, kth, NQ, with_cost, red_out, counter);
+  if (red_out) finish_partials(partials, NG, kth, NQ, with_cost, red_out, counter, p2p.world > 1 ? &p2p : nullptr);
 }
 
 // ---------------------------------------------------------------------------

@@ -115,7 +115,7 @@ tile_hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restr
                      const double2* __restrict__ coef, const double2* __restrict__ hv, double hv_scale, int L,
                      int n, int64_t c0, int64_t C, const int64_t* __restrict__ cidx, double2* __restrict__ scratch,
                      double* __restrict__ out_terms, double* __restrict__ partials, int with_cost,
-                     double* __restrict__ red_out, unsigned* __restrict__ counter) {  // TN amplitudes (dynamic: > 48 KB)
+                     double* __restrict__ red_out, unsigned* __restrict__ counter, P2PArgs p2p) {  // TN amplitudes (dynamic: > 48 KB)
   double2* s = dvqls_smem;
   __shared__ double red[THREADS / 32];
   __shared__ double acc4[4];
@@ -284,7 +284,7 @@ tile_hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restr
     double* o = partials + ((size_t)kth * G + blockIdx.x) * 4;
     o[0] = acc4[0]; o[1] = acc4[1]; o[2] = acc4[2]; o[3] = acc4[3];
   }
-  if (red_out) finish_partials(partials, G, kth, n, with_cost, red_out, counter);
+  if (red_out) finish_partials(partials, G, kth, n, with_cost, red_out, counter, p2p.world > 1 ? &p2p : nullptr);
 }
 
 // ---------------------------------------------------------------------------
