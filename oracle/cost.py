@@ -58,3 +58,17 @@ def cost(terms: np.ndarray, coeffs, n: int, L: int):
 
 def coeffs_of(w) -> np.ndarray:
     return np.array([c for c, _ in w.terms], dtype=np.complex128)
+
+
+def global_cost(overlaps: np.ndarray, coeffs, Psi: complex) -> float:
+    """NEXT-3, Eq. 1 (P:349-351): C_G = 1 - |<b|A|x>|^2 / <x|A^+A|x>, with
+    <b|A|x> = sum_l c_l beta_l (beta_l = Re + i Im of the overlap Hadamard tests) and
+    <x|A^+A|x> = Re Psi, the local cost's denominator sum (Alg. 1 Step 4b)."""
+    c = np.asarray(coeffs, dtype=np.complex128)
+    beta = np.asarray(overlaps[0::2]) + 1j * np.asarray(overlaps[1::2])
+    s = 0j
+    for l in range(len(c)):
+        s += c[l] * beta[l]
+    if Psi.real <= 1e-12:
+        raise DegenerateDenominator(f"Re Psi = {Psi.real} <= 1e-12")
+    return 1.0 - abs(s) ** 2 / Psi.real

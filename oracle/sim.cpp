@@ -69,6 +69,18 @@ void apply_c1q(State& psi, int m, int c, int q, const Gate2& U) {
   }
 }
 
+// single-qubit gate U on qubit q, controlled on qubits c1 and c2 both being |1>
+void apply_cc1q(State& psi, int m, int c1, int c2, int q, const Gate2& U) {
+  const size_t s = size_t(1) << bitpos(m, q);
+  const size_t cm = (size_t(1) << bitpos(m, c1)) | (size_t(1) << bitpos(m, c2));
+  for (size_t i = 0; i < psi.size(); ++i) {
+    if ((i & s) || (i & cm) != cm) continue;
+    cplx a = psi[i], b = psi[i | s];
+    psi[i] = U.u00 * a + U.u01 * b;
+    psi[i | s] = U.u10 * a + U.u11 * b;
+  }
+}
+
 // controlled dense unitary U (2^n x 2^n, row-major) on system qubits 1..n,
 // control = ancilla (qubit 0, the MSB): acts on the anc=1 half only.
 void apply_c_dense(State& psi, int n, const std::vector<cplx>& U) {
@@ -119,6 +131,22 @@ void apply_ansatz(State& psi, int m, int offset, const Problem& P, const double*
         apply_c1q(psi, m, c, tq, P.entangler == 0 ? kX : kZ);
       }
     }
+  }
+}
+
+// V(theta) on the system qubits (register qubits 1..n), every gate controlled on the ancilla
+// (qubit 0): c-Ry, c-Rz, c-Ry per qubit, the ring as Toffoli (CNOT) or CCZ (CZ) gates.
+void apply_controlled_ansatz(State& psi, const Problem& P, const double* theta) {
+  const int n = P.n, m = n + 1;
+  for (int layer = 0; layer < P.layers; ++layer) {
+    for (int q = 0; q < n; ++q) {
+      const double* t = theta + (layer * n + q) * 3;
+      apply_c1q(psi, m, 0, q + 1, Ry(t[0]));
+      apply_c1q(psi, m, 0, q + 1, Rz(t[1]));
+      apply_c1q(psi, m, 0, q + 1, Ry(t[2]));
+    }
+    if (n >= 2)
+      for (int q = 0; q < n; ++q) apply_cc1q(psi, m, 0, q + 1, (q + 1) % n + 1, P.entangler == 0 ? kX : kZ);
   }
 }
 
@@ -180,6 +208,23 @@ double hadamard_test(const Problem& P, const double* theta, const State* prefix,
     apply_controlled_Ub(psi, P, /*dagger=*/false);
   }
   apply_controlled_pauli_string(psi, m, P.paulis[l]);
+  apply_1q(psi, m, 0, kH);
+  return expect_z_anc(psi);
+}
+
+// Global-cost overlap Hadamard test (NEXT-3; Eq. 1): Re (part 0) or Im (part 1)
+// of beta_l = <0| U_b^+ A_l V(theta) |0> = <b| A_l |x>, gate by gate on n+1 qubits:
+// |0..0>, H(anc), [S^+(anc)], controlled V(theta), controlled A_l, controlled U_b^+, H(anc),
+// <Z_anc>.  (The |0> branch keeps |0^n>; the |1> branch carries U_b^+ A_l V|0>.)
+double overlap_test(const Problem& P, const double* theta, int l, int part) {
+  const int n = P.n, m = n + 1;
+  State psi(size_t(1) << m, 0);
+  psi[0] = 1;
+  apply_1q(psi, m, 0, kH);
+  if (part == 1) apply_1q(psi, m, 0, kSdg);
+  apply_controlled_ansatz(psi, P, theta);
+  apply_controlled_pauli_string(psi, m, P.paulis[l]);
+  apply_controlled_Ub(psi, P, /*dagger=*/true);
   apply_1q(psi, m, 0, kH);
   return expect_z_anc(psi);
 }
@@ -274,6 +319,27 @@ int oracle_terms(int n, int layers, int L, const char* paulis, int entangler, in
         const int64_t c = idx ? idx[i] : i;
         out[i] = hadamard_test(P, theta, mode == 1 ? &prefix : nullptr, c);
       }
+    });
+  }
+  for (auto& th : pool) th.join();
+  return 0;
+}
+
+// NEXT-3: the 2L overlap Hadamard tests, out[2l + part] = Re / Im <b|A_l|x>.
+int oracle_overlap_terms(int n, int layers, int L, const char* paulis, int entangler, int bkind,
+                         const double* b_amps, const double* theta, int nthreads, double* out) {
+  Problem P;
+  int rc = build_problem(P, n, layers, L, paulis, entangler, bkind, b_amps);
+  if (rc) return rc;
+  const int64_t count = 2 * int64_t(L);
+  if (nthreads < 1) nthreads = int(std::thread::hardware_concurrency());
+  if (nthreads < 1) nthreads = 1;
+  if (int64_t(nthreads) > count) nthreads = int(count);
+  std::vector<std::thread> pool;
+  for (int w = 0; w < nthreads; ++w) {
+    pool.emplace_back([&, w]() {
+      const int64_t lo = count * w / nthreads, hi = count * (w + 1) / nthreads;
+      for (int64_t i = lo; i < hi; ++i) out[i] = overlap_test(P, theta, int(i / 2), int(i % 2));
     });
   }
   for (auto& th : pool) th.join();

@@ -46,6 +46,9 @@ def lib():
             L.oracle_ub_matrix.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp]
             L.oracle_ub_matrix.restype = ctypes.c_int
             L.oracle_hardware_threads.restype = ctypes.c_int
+            L.oracle_overlap_terms.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                                               ctypes.c_int, ctypes.c_int, dp, dp, ctypes.c_int, dp]
+            L.oracle_overlap_terms.restype = ctypes.c_int
             _lib = L
     return _lib
 
@@ -111,3 +114,24 @@ def workload_terms(w, theta=None, mode=1, nthreads=0, idx=None) -> np.ndarray:
     chars, _ = w.arrays()
     th = w.theta0() if theta is None else theta
     return terms(w.n, w.layers, chars, th, w.bkind, w.b, w.entangler, mode, nthreads, idx)
+
+
+def overlap_terms(n, layers, paulis: bytes, theta, bkind=0, b=None, entangler=0, nthreads=0) -> np.ndarray:
+    """NEXT-3: 2L values, [2l + part] = Re / Im <b|A_l|x> from the gate-by-gate overlap
+    Hadamard test (controlled V, controlled A_l, controlled U_b^+)."""
+    L = len(paulis) // n
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    assert theta.size == 3 * n * layers
+    bamps = _interleave(b) if (bkind == 1) else None
+    out = np.empty(2 * L, dtype=np.float64)
+    rc = lib().oracle_overlap_terms(n, layers, L, paulis, entangler, bkind, _dp(bamps), _dp(theta), nthreads,
+                                    _dp(out))
+    if rc != 0:
+        raise ValueError(f"oracle_overlap_terms failed rc={rc}")
+    return out
+
+
+def workload_overlaps(w, theta=None, nthreads=0) -> np.ndarray:
+    chars, _ = w.arrays()
+    th = w.theta0() if theta is None else theta
+    return overlap_terms(w.n, w.layers, chars, th, w.bkind, w.b, w.entangler, nthreads)
