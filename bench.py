@@ -56,10 +56,19 @@ def fp64_ops_per_eval(w, circuits=None):
 
 
 def hbm_bytes_per_eval(w, circuits=None):
-    """Streaming-path algorithmic HBM bytes (SURVEY §8(d) "streaming model", n > 12):
-    numerator circuit 3 passes = 96 N B (P1 reads x / writes phi, P2 reads+writes phi,
-    P3 reads phi and x), denominator 32 N B."""
-    return smem_bytes_per_eval(w, circuits)
+    """Streaming-path algorithmic DRAM bytes (n > 12, stream.cuh): the branch of a numerator
+    circuit makes 3 passes through its per-CTA scratch (P0 writes 16N, P1 reads + writes 32N,
+    P2 reads 16N: 64N) while x (<= 64 MB for n <= 22) stays L2-resident; n >= 23 takes 5 passes
+    (128N) and x (128-256 MB) is read from DRAM twice (32N, also by the denominators).
+    SURVEY §8(d) counts x as HBM traffic too (96N); that figure is reported beside it."""
+    N = 1 << w.n
+    c = np.arange(w.n_circuits) if circuits is None else circuits
+    s = (c // 2) % (w.n + 1)
+    num = int(np.count_nonzero(s))
+    den = c.size - num
+    if w.n <= 22:
+        return num * 64 * N
+    return num * 160 * N + den * 32 * N
 
 
 def smem_bytes_per_eval(w, circuits=None):
@@ -158,15 +167,47 @@ def traffic_from_profiles():
     return None
 
 
-def streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src):
+def streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, grid=None):
     b = hbm_bytes_per_eval(w, local_c) * KT
+    b96 = smem_bytes_per_eval(w, local_c) * KT
     ach = b / (had_ms * 1e-3)
     peak = float(peaks["hbm_gbs"]) * 1e9
-    return {"bound": "hbm", "kernel": "tile_hadamard_kernel", "achieved": ach / 1e9, "peak": peak / 1e9,
-            "unit": "GB/s", "frac": ach / peak, "traffic": None,
-            "note": (f"algorithmic HBM bytes per launch = {b:.4g} (96N per numerator circuit, 32N per "
-                     f"denominator, SURVEY §8(d) streaming model) / mean CUDA-event kernel time; peak = "
-                     f"hbm_gbs of {peak_src} MEASURED_PEAKS.json; n > 21 runs 5 passes (160N)")}
+    out = {"bound": "hbm", "kernel": "stream_hadamard_kernel<12>", "achieved": ach / 1e9, "peak": peak / 1e9,
+           "unit": "GB/s", "frac": ach / peak, "traffic": None,
+           "model96_GBps": b96 / (had_ms * 1e-3) / 1e9,
+           "note": (f"algorithmic DRAM bytes per launch = {b:.4g} (64N per numerator circuit: 3 passes "
+                    f"through the per-CTA scratch, x L2-resident; n >= 23: 160N + 32N per denominator) / mean "
+                    f"CUDA-event kernel time; peak = hbm_gbs of {peak_src} MEASURED_PEAKS.json. model96_GBps "
+                    f"= the SURVEY §8(d) 96N model (x reads counted as HBM)")}
+    if grid is not None:
+        scratch = grid * (1 << w.n) * 16
+        out["scratch_bytes"] = scratch
+        if scratch <= 100 << 20:
+            out["note"] += "; the per-CTA scratch fits in L2 at this n, so L2 bandwidth, not HBM, bounds it"
+    return out
+
+
+def onchip_roofline(w, local_c, KT, had_ms, sms, fmax, peak_src):
+    """n = 11, 12 (stream.cuh single tile): FP64-pipe ops vs 64 lanes/clk/SM; on-chip bytes =
+    4 SMEM exchanges per numerator circuit (STS + LDS of the 16N-byte branch each: 128N) plus x
+    gathered twice from L1/L2 (32N, not SMEM)."""
+    ops = fp64_ops_per_eval(w, local_c) * KT
+    N = 1 << w.n
+    s = (local_c // 2) % (w.n + 1)
+    num = int(np.count_nonzero(s))
+    sbytes = num * 128 * N * KT
+    fp64_peak = 64 * sms * fmax
+    smem_peak = 128 * sms * fmax
+    t = had_ms * 1e-3
+    return {"bound": "alu", "kernel": f"stream_hadamard_kernel<{11 if w.n == 11 else 12}>",
+            "achieved": ops / t / 1e12, "peak": fp64_peak / 1e12, "unit": "Top/s", "frac": ops / t / fp64_peak,
+            "traffic": None,
+            "smem": {"achieved": sbytes / t / 1e9, "peak": smem_peak / 1e9, "unit": "GB/s",
+                     "frac": sbytes / t / smem_peak,
+                     "note": "4 exchanges (STS + LDS) of the branch per numerator circuit = 128N bytes"},
+            "model_frac": max(ops / fp64_peak, sbytes / smem_peak) / t,
+            "note": (f"FP64-pipe lane-ops per launch = {ops:.4g} / mean CUDA-event kernel time; peak = 64 "
+                     f"lanes/clk/SM x {sms} SMs x sm_max_mhz ({peak_src} MEASURED_PEAKS.json)")}
 
 
 # ----------------------------------------------------------------------------------------------
@@ -248,6 +289,7 @@ def main():
     ap.add_argument("--n", type=int, default=16, help="qubits for --config cfg5 (12..24)")
     ap.add_argument("--impl", default="dvqls", choices=["dvqls", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-next2", action="store_true", help="skip the NEXT-2 fast-path side measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = CONFIGS[args.config](args.n) if args.config == "cfg5" else CONFIGS[args.config]()
@@ -387,6 +429,36 @@ def main():
     barrier()
     e2e_s = max_over_ranks(e2e_s)
 
+    # ---- NEXT-2 algebraic fast path (flagged; reported separately, never the headline) ----------
+    next2 = None
+    if w.bkind == 0 and not args.no_next2:
+        pctx = dvqls.Context(w.n, w.layers, chars, co, w.bkind, w.b, device=local, rank=rank, world=world,
+                             nccl_id=nccl_id, entangler=w.entangler, stream=stream, timing=False,
+                             max_batch=max(KT, 1), mode=dvqls.DVQLS_MODE_PAULI)
+        p_steps = max(3, args.steps // 4)
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                flush.zero_()
+                pctx.cost_dev(KT, th_dev, out_dev)
+            barrier()
+            ps = [torch.cuda.Event(enable_timing=True) for _ in range(p_steps)]
+            pe = [torch.cuda.Event(enable_timing=True) for _ in range(p_steps)]
+            for i in range(p_steps):
+                flush.zero_()
+                ps[i].record(stream)
+                pctx.cost_dev(KT, th_dev, out_dev)
+                pe[i].record(stream)
+            barrier()
+        p_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in zip(ps, pe)))
+        pres = out_dev.view(KT, 5).cpu().numpy()
+        next2 = {"evals_per_s": KT * p_steps / (p_ms * 1e-3), "ms_per_step": p_ms / p_steps,
+                 "observables": pctx.num_observables(), "tasks": w.n_tasks,
+                 "max_abs_cost_diff_vs_circuits": float(np.max(np.abs(pres[:, 0] - res[:, 0]))),
+                 "note": ("NEXT-2 algebraic fast path (DVQLS_MODE_PAULI): U_b Z_j U_b^+ = X_j, each distinct "
+                          "Pauli observable evaluated once per theta, Re/Im shared. Flagged: not circuits/s, "
+                          "not the headline (SURVEY §8(d) headline rules)")}
+        pctx.destroy()
+
     # ---- derived numbers -------------------------------------------------------------------------
     circuits_step = w.n_circuits * KT
     value = circuits_step * args.steps / (dev_ms * 1e-3)
@@ -434,7 +506,8 @@ def main():
                                  "reduce": statistics.mean(t["reduce_ms"] for t in k1t)},
                    "note": "one cost evaluation per step (same loop, same L2 flush)"},
             "kernel_ms": {"prefix": pre_ms, "hadamard": had_ms, "reduce": red_ms},
-            "roofline": streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src) if w.n > 12 else {
+            "roofline": streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, ctx.grid()) if w.n > 12 else
+            onchip_roofline(w, local_c, KT, had_ms, sms, fmax, peak_src) if w.n > 10 else {
                 "bound": "alu",
                 "kernel": "hadamard_kernel",
                 "achieved": achieved_ops / 1e12,
@@ -457,6 +530,7 @@ def main():
             "clocks": clocks,
             "cost": float(res[0, 0]),
             "cost_k1": float(res1[0]),
+            "next2_pauli": next2,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(w, thetas[0])

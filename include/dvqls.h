@@ -64,6 +64,16 @@ typedef struct dvqls_bprep {
                           copied at create.  Ignored for UNIFORM.                       */
 } dvqls_bprep;
 
+/* ---- evaluation mode (dvqls_opts.mode) --------------------------------- */
+#define DVQLS_MODE_CIRCUITS 0 /* every Hadamard-test circuit simulated on its own (the
+                                 method as stated; the headline path)          */
+#define DVQLS_MODE_PAULI 1    /* NEXT-2 algebraic fast path, FLAGGED: uniform b only.
+                                 U_b Z_j U_b^+ = X_j (P:382 with U_b = H^n), every term is
+                                 i^q <x|P|x> of one Pauli string P = A_l X_j A_k (or
+                                 A_l A_k); each distinct P is evaluated once per theta and
+                                 Re/Im share it.  Same outputs as CIRCUITS up to rounding;
+                                 never reported as circuits/s.                             */
+
 /* ---- options (all fields optional: pass NULL for defaults) ------------- */
 typedef struct dvqls_opts {
   int device;                  /* CUDA device ordinal; -1 = current device              */
@@ -75,6 +85,7 @@ typedef struct dvqls_opts {
   void* cuda_stream;           /* cudaStream_t for all device work; NULL = library-owned */
   int timing;                  /* nonzero: record CUDA events around each kernel         */
   int max_batch;               /* largest K accepted by the *_batch calls (default 16)   */
+  int mode;                    /* DVQLS_MODE_CIRCUITS (0, default) or DVQLS_MODE_PAULI   */
 } dvqls_opts;
 
 typedef struct dvqls_ctx dvqls_ctx;
@@ -148,6 +159,19 @@ const char* dvqls_last_error(const dvqls_ctx* ctx); /* "" if none; static text i
 int64_t dvqls_num_circuits(const dvqls_ctx* ctx);   /* 2(n+1)L^2 */
 int dvqls_local_range(const dvqls_ctx* ctx, int64_t* c0, int64_t* c1);
 void* dvqls_stream(const dvqls_ctx* ctx);           /* the cudaStream_t in use */
+/* CTAs of the Hadamard-test kernel per theta (the n >= 13 streaming path: in total over the
+ * batch, one 2^n-amplitude scratch each). */
+int dvqls_launch_grid(const dvqls_ctx* ctx);
+/* DVQLS_MODE_PAULI: number of distinct Pauli observables among the (n+1)L^2 tasks
+ * (0 in CIRCUITS mode). */
+int64_t dvqls_num_observables(const dvqls_ctx* ctx);
+/* Pure host helper (no device access), NEXT-2 algebra: the observable of task (l, k, s) for
+ * uniform b, B = A_l X_j A_k (s = 1 + j) or A_l A_k (s = 0), as
+ *     B|i> = i^phase (-1)^{popcount(i & z_mask)} |i ^ x_mask>   (big-endian bits).
+ *   pauli_l, pauli_k  n characters each from {I,X,Y,Z}
+ * Returns DVQLS_E_ARG / DVQLS_E_PAULI on bad input. */
+int dvqls_task_observable(int n, const char* pauli_l, const char* pauli_k, int s, uint32_t* x_mask,
+                          uint32_t* z_mask, int* phase);
 /* Kernel launches per cost evaluation call (prefix + circuits + reduce [+ finalize]). */
 int dvqls_launches_per_call(const dvqls_ctx* ctx);
 /* With opts.timing: device milliseconds of the last call, measured with CUDA events

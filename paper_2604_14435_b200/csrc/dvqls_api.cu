@@ -16,12 +16,15 @@
 #include <cstdlib>
 #include <cstring>
 #include <set>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
 #include "../../include/dvqls.h"
 #include "kernels.cuh"
 #include "tile.cuh"
+#include "stream.cuh"
+#include "pauli.cuh"
 #include "nccl_dl.h"
 
 using namespace dvqls;
@@ -124,7 +127,8 @@ struct dvqls_ctx {
   std::vector<char*> peer_ptrs;
   char** d_peers = nullptr;
   unsigned long long epoch = 0;
-  bool tile_path = false;        // n > 10
+  bool tile_path = false;        // n > 10 (stream.cuh)
+  int tile_bits = 12;            // tile path: amplitudes per SMEM tile = 2^tile_bits
   double2* d_scratch = nullptr;  // grid * N (n > 12)
   double2* d_x2 = nullptr;       // ring ping-pong buffer (n > 12 prefix)
   double2* d_gates = nullptr;    // fused-gate table (n > 12 prefix)
@@ -132,6 +136,17 @@ struct dvqls_ctx {
   double* d_sub = nullptr;
   int64_t sub_cap = 0;
   size_t h_stage_bytes = 0;
+
+  // NEXT-2 algebraic fast path (opts.mode = DVQLS_MODE_PAULI; pauli.cuh)
+  int mode = DVQLS_MODE_CIRCUITS;
+  int64_t D = 0, d0 = 0, d1 = 0;  // distinct observables; this rank's block [d0, d1)
+  int pgrid = 0;                  // CTAs of pauli_expect_kernel per theta (cost path)
+  pauli::Obs* d_obs = nullptr;
+  double2* d_wE = nullptr;        // per observable: sum of c_l^* c_k i^q over numerator tasks
+  double2* d_wP = nullptr;        // ... over denominator tasks
+  uint32_t* d_task = nullptr;     // per task: (observable << 2) | q
+  double2* d_e = nullptr;         // D expectations of the last terms call
+  size_t pauli_smem = 0;
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   bool timed_once = false;
@@ -167,12 +182,24 @@ int fail(dvqls_ctx* c, int code, const char* fmt, ...) {
 
 thread_local std::string g_create_err;
 
-// Hadamard-test kernel over circuits [c0, c0 + C) (or the list cidx[0..C)) of every theta.
-// red_out != NULL: the kernel's last CTA per theta also performs the fixed-order reduction
-// (with_cost: 5 doubles C, E, Psi per theta; else 4 doubles E, Psi for the allreduce).
-int launch_hadamard(dvqls_ctx* ctx, int K, int64_t c0, int64_t C, const int64_t* cidx, double* terms, int grid,
-                    double* red_out = nullptr, int with_cost = 0) {
-  dim3 g(grid, K);
+// Symbolic product of Pauli operators in the representation P|i> = i^q (-1)^{popcount(i & z)}
+// |i ^ m>:  (Q P)|i> = i^{q_P + q_Q + 2 popcount(m_P & z_Q)} (-1)^{i . (z_P ^ z_Q)} |i ^ m_P ^ m_Q>.
+struct PauliOp {
+  uint32_t m, z;
+  int q;
+};
+PauliOp pauli_mul(const PauliOp& Q, const PauliOp& P) {  // Q * P (P applied first)
+  return PauliOp{P.m ^ Q.m, P.z ^ Q.z, (P.q + Q.q + 2 * __builtin_popcount(P.m & Q.z)) & 3};
+}
+// Observable of task (l, k, s) for uniform b (NEXT-2): A_l X_j A_k (s = 1 + j) or A_l A_k (s = 0),
+// X_j on system qubit j = index bit n - 1 - j (U_b Z_j U_b^+ = H Z H = X)
+PauliOp task_observable(int n, const PauliTerm& Tl, const PauliTerm& Tk, int s) {
+  PauliOp r{Tk.xm, Tk.zm, Tk.ny & 3};
+  if (s > 0) r = pauli_mul(PauliOp{1u << (n - 1 - (s - 1)), 0u, 0}, r);
+  return pauli_mul(PauliOp{Tl.xm, Tl.zm, Tl.ny & 3}, r);
+}
+
+P2PArgs make_p2p(dvqls_ctx* ctx, double* red_out, int with_cost) {
   P2PArgs p2p{1, 0, ctx->max_batch, 0ull, nullptr};
   if (red_out && with_cost && ctx->p2p) {
     p2p.world = ctx->world;
@@ -180,6 +207,30 @@ int launch_hadamard(dvqls_ctx* ctx, int K, int64_t c0, int64_t C, const int64_t*
     p2p.epoch = ++ctx->epoch;
     p2p.peers = ctx->d_peers;
   }
+  return p2p;
+}
+
+// NEXT-2: distinct observables [d0, d1) of every theta; e -> out_e (nullable), fused reduction
+int launch_pauli(dvqls_ctx* ctx, int K, int64_t d0, int64_t d1, double2* out_e, int grid, double* red_out,
+                 int with_cost) {
+  P2PArgs p2p = make_p2p(ctx, red_out, with_cost);
+  const int stage = ctx->pauli_smem > 0 ? 1 : 0;
+  void* args[] = {(void*)&ctx->d_x, (void*)&ctx->n, (void*)&ctx->d_obs, (void*)&ctx->d_wE, (void*)&ctx->d_wP,
+                  (void*)&d0, (void*)&d1, (void*)&ctx->D, (void*)&out_e, (void*)&ctx->d_partials,
+                  (void*)&with_cost, (void*)&red_out, (void*)&ctx->d_counter, (void*)&p2p, (void*)&stage};
+  CK(cudaLaunchKernel((const void*)&pauli::pauli_expect_kernel, dim3(grid, K), dim3(pauli::WARPS * 32), args,
+                      ctx->pauli_smem, ctx->stream));
+  return DVQLS_OK;
+}
+
+// Hadamard-test kernel over circuits [c0, c0 + C) (or the list cidx[0..C)) of every theta.
+// red_out != NULL: the kernel's last CTA per theta also performs the fixed-order reduction
+// (with_cost: 5 doubles C, E, Psi per theta; else 4 doubles E, Psi for the allreduce).
+int launch_hadamard(dvqls_ctx* ctx, int K, int64_t c0, int64_t C, const int64_t* cidx, double* terms, int grid,
+                    double* red_out = nullptr, int with_cost = 0) {
+  if (ctx->tile_path && ctx->n > ctx->tile_bits) grid = std::max(1, grid / K);  // scratch: grid CTAs in total
+  dim3 g(grid, K);
+  P2PArgs p2p = make_p2p(ctx, red_out, with_cost);
   if (!ctx->tile_path) {
     void* args[] = {(void*)&ctx->d_x,   (void*)&ctx->d_tab, (void*)&ctx->d_coef,  (void*)&ctx->d_hv,
                     (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&c0, (void*)&C,
@@ -238,8 +289,22 @@ int launch_eval(dvqls_ctx* ctx, int K, const double* thetas_dev, bool want_cost,
     // a9 (+ a10 on one rank) fused into the kernel tail (last-CTA fixed-order reduction)
     const bool direct = ctx->world == 1 || ctx->p2p;  // kernel writes the final (C, E, Psi)
     double* red = want_cost ? (direct ? out_dev : ctx->d_ep) : nullptr;
-    int rc = launch_hadamard(ctx, K, ctx->c0, Cloc, nullptr, ctx->d_terms, ctx->grid, red, direct ? 1 : 0);
-    if (rc) return rc;
+    if (ctx->mode == DVQLS_MODE_PAULI) {
+      int rc;
+      if (want_cost) {
+        rc = launch_pauli(ctx, K, ctx->d0, ctx->d1, nullptr, ctx->pgrid, red, direct ? 1 : 0);
+      } else {  // terms: every observable on every rank (cheap), then this rank's circuit block
+        rc = launch_pauli(ctx, K, 0, ctx->D, ctx->d_e, ctx->pgrid, nullptr, 0);
+        if (!rc) {
+          pauli::pauli_scatter_kernel<<<296, 256, 0, ctx->stream>>>(ctx->d_e, ctx->d_task, ctx->c0, Cloc, ctx->d_terms);
+          CK(cudaGetLastError());
+        }
+      }
+      if (rc) return rc;
+    } else {
+      int rc = launch_hadamard(ctx, K, ctx->c0, Cloc, nullptr, ctx->d_terms, ctx->grid, red, direct ? 1 : 0);
+      if (rc) return rc;
+    }
   }
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
   if (want_cost) {
@@ -264,6 +329,7 @@ void release(dvqls_ctx* c) {
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
   cudaFree(c->d_tab); cudaFree(c->d_coef); cudaFree(c->d_hv); cudaFree(c->d_theta); cudaFree(c->d_x);
   cudaFree(c->d_terms); cudaFree(c->d_partials); cudaFree(c->d_ep); cudaFree(c->d_out); cudaFree(c->d_gather);
+  cudaFree(c->d_obs); cudaFree(c->d_wE); cudaFree(c->d_wP); cudaFree(c->d_task); cudaFree(c->d_e);
   cudaFree(c->d_counter); cudaFree(c->d_scratch); cudaFree(c->d_x2); cudaFree(c->d_gates); cudaFree(c->d_cidx); cudaFree(c->d_sub);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
@@ -353,7 +419,7 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   ctx->n = n; ctx->layers = layers; ctx->L = L; ctx->P = 3 * n * layers; ctx->N = 1 << n;
   if (opts) {
     ctx->device = opts->device; ctx->rank = opts->rank; ctx->world = opts->world;
-    ctx->entangler = opts->entangler; ctx->timing = opts->timing;
+    ctx->entangler = opts->entangler; ctx->timing = opts->timing; ctx->mode = opts->mode;
     if (opts->max_batch > 0) ctx->max_batch = opts->max_batch;
   } else {
     ctx->device = -1; ctx->rank = 0; ctx->world = 1;
@@ -367,6 +433,14 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   if (ctx->world < 1 || ctx->rank < 0 || ctx->rank >= ctx->world) {
     fail(ctx, DVQLS_E_ARG, "rank/world out of range");
     return bail(DVQLS_E_ARG);
+  }
+  if (ctx->mode != DVQLS_MODE_CIRCUITS && ctx->mode != DVQLS_MODE_PAULI) {
+    fail(ctx, DVQLS_E_ARG, "mode must be DVQLS_MODE_CIRCUITS or DVQLS_MODE_PAULI");
+    return bail(DVQLS_E_ARG);
+  }
+  if (ctx->mode == DVQLS_MODE_PAULI && bprep && bprep->kind != DVQLS_B_UNIFORM) {
+    fail(ctx, DVQLS_E_UNSUPPORTED, "the Pauli fast path needs uniform b (U_b Z_j U_b^+ = X_j)");
+    return bail(DVQLS_E_UNSUPPORTED);
   }
   if (ctx->entangler != 0 && ctx->entangler != 1) {
     fail(ctx, DVQLS_E_ARG, "entangler must be 0 (CNOT ring) or 1 (CZ ring)");
@@ -464,11 +538,17 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   if (!ctx->tile_path) {
     ctx->kc = ctx->bkind == DVQLS_B_AMPLITUDES ? cfg_for<true>(n) : cfg_for<false>(n);
   } else {
-    ctx->kc.fn = ctx->bkind == DVQLS_B_AMPLITUDES ? (const void*)&tile::tile_hadamard_kernel<true>
-                                                  : (const void*)&tile::tile_hadamard_kernel<false>;
-    ctx->kc.warps = tile::THREADS / 32;
+    const bool hh = ctx->bkind == DVQLS_B_AMPLITUDES;
+    ctx->tile_bits = n == 11 ? 11 : 12;
+    if (ctx->tile_bits == 11)
+      ctx->kc.fn = hh ? (const void*)&stream::stream_hadamard_kernel<11, true>
+                      : (const void*)&stream::stream_hadamard_kernel<11, false>;
+    else
+      ctx->kc.fn = hh ? (const void*)&stream::stream_hadamard_kernel<12, true>
+                      : (const void*)&stream::stream_hadamard_kernel<12, false>;
+    ctx->kc.warps = (1 << ctx->tile_bits) / 16 / 32;
     ctx->kc.gpw = 1;
-    ctx->kc.smem = sizeof(double2) * tile::TN;
+    ctx->kc.smem = sizeof(double2) * (size_t(1) << ctx->tile_bits);
   }
   if (cudaFuncSetAttribute(ctx->kc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->kc.smem)) !=
       cudaSuccess) {
@@ -488,13 +568,72 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   const int64_t Cloc = ctx->c1 - ctx->c0;
   const int64_t groups_per_cta = ctx->tile_path ? 1 : int64_t(ctx->kc.warps) * ctx->kc.gpw;
   int64_t want = int64_t(prop.multiProcessorCount) * occ;
-  if (ctx->tile_path && n > 12) {  // each CTA owns a 2^n-amplitude global scratch
+  if (ctx->tile_path && n > ctx->tile_bits) {  // each CTA owns a 2^n-amplitude global scratch
     const int64_t cap = int64_t(kScratchBudget / (sizeof(double2) * size_t(ctx->N)));
     want = std::max<int64_t>(1, std::min(want, cap));
+  }
+  if (ctx->tile_path) {
+    const char* e = getenv("DVQLS_STREAM_GRID");  // tuning knob: CTAs of the n >= 11 path
+    if (e && atoi(e) > 0) want = std::min<int64_t>(want, atoi(e));
   }
   const int64_t need = (Cloc + groups_per_cta - 1) / groups_per_cta;
   ctx->grid = int(std::max<int64_t>(1, std::min(want, need)));
   ctx->NG = int64_t(ctx->grid) * groups_per_cta;
+
+  // ---- NEXT-2: symbolic task observables, dedup, folded weights (pauli.cuh) ---------------
+  std::vector<pauli::Obs> obs;
+  std::vector<double2> wE, wP;
+  std::vector<uint32_t> task;
+  if (ctx->mode == DVQLS_MODE_PAULI) {
+    const int64_t T = ctx->C / 2;
+    if (T > (int64_t(1) << 30)) {
+      fail(ctx, DVQLS_E_UNSUPPORTED, "too many tasks for the Pauli fast path");
+      return bail(DVQLS_E_UNSUPPORTED);
+    }
+    std::unordered_map<uint64_t, uint32_t> index;
+    task.resize(size_t(T));
+    for (int64_t t = 0; t < T; ++t) {
+      const int s_ = int(t % (n + 1));
+      const int64_t lk = t / (n + 1);
+      const int k = int(lk % L), l = int(lk / L);
+      const PauliOp B = task_observable(n, tab[l], tab[k], s_);
+      const uint64_t key = (uint64_t(B.m) << 32) | B.z;
+      auto it = index.find(key);
+      uint32_t d;
+      if (it == index.end()) {
+        d = uint32_t(obs.size());
+        index.emplace(key, d);
+        obs.push_back(pauli::Obs{B.m, B.z});
+        wE.push_back(make_double2(0.0, 0.0));
+        wP.push_back(make_double2(0.0, 0.0));
+      } else {
+        d = it->second;
+      }
+      task[size_t(t)] = (d << 2) | uint32_t(B.q);
+      // weight c_l^* c_k i^q (E = sum w <x|B|x> = sum w i^q e)
+      const std::complex<double> w = std::conj(std::complex<double>(coef[l].x, coef[l].y)) *
+                                     std::complex<double>(coef[k].x, coef[k].y) *
+                                     std::pow(std::complex<double>(0.0, 1.0), B.q);
+      double2& acc = s_ == 0 ? wP[d] : wE[d];
+      acc.x += w.real();
+      acc.y += w.imag();
+    }
+    ctx->D = int64_t(obs.size());
+    dvqls_shard_range(ctx->D, ctx->rank, ctx->world, &ctx->d0, &ctx->d1);
+    ctx->pauli_smem = ctx->N <= 8192 ? sizeof(double2) * size_t(ctx->N) : 0;
+    if (cudaFuncSetAttribute((const void*)&pauli::pauli_expect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(ctx->pauli_smem)) != cudaSuccess) {
+      fail(ctx, DVQLS_E_CUDA, "pauli kernel smem");
+      return bail(DVQLS_E_CUDA);
+    }
+    int pocc = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pocc, (const void*)&pauli::pauli_expect_kernel,
+                                                  pauli::WARPS * 32, ctx->pauli_smem);
+    const int64_t pw = int64_t(prop.multiProcessorCount) * std::max(1, pocc);
+    const int64_t pneed = (ctx->D + pauli::WARPS - 1) / pauli::WARPS;  // terms launches cover all D
+    ctx->pgrid = int(std::max<int64_t>(1, std::min(pw, pneed)));
+    ctx->NG = std::max<int64_t>(ctx->NG, ctx->pgrid);
+  }
 
   {
     const char* e = getenv("DVQLS_PREFIX_RB");  // tuning knob: register-phase prefix for n <= 10
@@ -550,7 +689,14 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
       alloc((void**)&ctx->d_ep, sizeof(double) * KB * 4) || alloc((void**)&ctx->d_out, sizeof(double) * KB * 5) ||
       (ctx->world > 1 && alloc((void**)&ctx->d_gather, sizeof(double) * ctx->world * ctx->chunk)) ||
       alloc((void**)&ctx->d_counter, sizeof(unsigned) * KB) ||
-      (n > 12 && alloc((void**)&ctx->d_scratch, sizeof(double2) * size_t(ctx->grid) * ctx->N)) ||
+      (n > 12 && ctx->mode == DVQLS_MODE_CIRCUITS &&
+       alloc((void**)&ctx->d_scratch, sizeof(double2) * size_t(ctx->grid) * ctx->N)) ||
+      (ctx->mode == DVQLS_MODE_PAULI &&
+       (alloc((void**)&ctx->d_obs, sizeof(pauli::Obs) * obs.size()) ||
+        alloc((void**)&ctx->d_wE, sizeof(double2) * obs.size()) ||
+        alloc((void**)&ctx->d_wP, sizeof(double2) * obs.size()) ||
+        alloc((void**)&ctx->d_task, sizeof(uint32_t) * task.size()) ||
+        alloc((void**)&ctx->d_e, sizeof(double2) * obs.size()))) ||
       (n > 12 && alloc((void**)&ctx->d_x2, sizeof(double2) * size_t(ctx->N))) ||
       (n > 12 && alloc((void**)&ctx->d_gates, sizeof(double2) * 2 * size_t(n) * layers))) {
     fail(ctx, DVQLS_E_CUDA, "cudaMalloc failed");
@@ -564,7 +710,12 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   if (cudaMemset(ctx->d_counter, 0, sizeof(unsigned) * KB) ||
       cudaMemcpy(ctx->d_tab, tab.data(), sizeof(PauliTerm) * L, cudaMemcpyHostToDevice) ||
       cudaMemcpy(ctx->d_coef, coef.data(), sizeof(double2) * L, cudaMemcpyHostToDevice) ||
-      (!hv.empty() && cudaMemcpy(ctx->d_hv, hv.data(), sizeof(double2) * ctx->N, cudaMemcpyHostToDevice))) {
+      (!hv.empty() && cudaMemcpy(ctx->d_hv, hv.data(), sizeof(double2) * ctx->N, cudaMemcpyHostToDevice)) ||
+      (!obs.empty() &&
+       (cudaMemcpy(ctx->d_obs, obs.data(), sizeof(pauli::Obs) * obs.size(), cudaMemcpyHostToDevice) ||
+        cudaMemcpy(ctx->d_wE, wE.data(), sizeof(double2) * obs.size(), cudaMemcpyHostToDevice) ||
+        cudaMemcpy(ctx->d_wP, wP.data(), sizeof(double2) * obs.size(), cudaMemcpyHostToDevice) ||
+        cudaMemcpy(ctx->d_task, task.data(), sizeof(uint32_t) * task.size(), cudaMemcpyHostToDevice)))) {
     fail(ctx, DVQLS_E_CUDA, "table upload failed");
     return bail(DVQLS_E_CUDA);
   }
@@ -706,7 +857,7 @@ int dvqls_terms_subset(dvqls_ctx* ctx, const double* theta, const int64_t* idx, 
   for (int64_t i = 0; i < count; ++i)
     if (idx[i] < 0 || idx[i] >= ctx->C) return fail(ctx, DVQLS_E_ARG, "circuit index %lld out of range", (long long)idx[i]);
   if (count == 0) return DVQLS_OK;
-  if (!ctx->tile_path || ctx->world > 1) {  // evaluate everything, pick the requested entries
+  if (!ctx->tile_path || ctx->world > 1 || ctx->mode == DVQLS_MODE_PAULI) {  // evaluate all, pick entries
     std::vector<double> all(size_t(ctx->C));
     int rc = dvqls_terms(ctx, theta, all.data());
     if (rc) return rc;
@@ -753,6 +904,39 @@ int dvqls_local_range(const dvqls_ctx* ctx, int64_t* c0, int64_t* c1) {
 }
 
 void* dvqls_stream(const dvqls_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int dvqls_launch_grid(const dvqls_ctx* ctx) {
+  if (!ctx) return DVQLS_E_ARG;
+  return ctx->mode == DVQLS_MODE_PAULI ? ctx->pgrid : ctx->grid;
+}
+
+int64_t dvqls_num_observables(const dvqls_ctx* ctx) {
+  if (!ctx) return DVQLS_E_ARG;
+  return ctx->mode == DVQLS_MODE_PAULI ? ctx->D : 0;
+}
+
+int dvqls_task_observable(int n, const char* pauli_l, const char* pauli_k, int s, uint32_t* x_mask,
+                          uint32_t* z_mask, int* phase) {
+  if (n < 1 || n > 24 || !pauli_l || !pauli_k || s < 0 || s > n || !x_mask || !z_mask || !phase) return DVQLS_E_ARG;
+  PauliTerm T[2] = {{0, 0, 0, 0u}, {0, 0, 0, 0u}};
+  const char* str[2] = {pauli_l, pauli_k};
+  for (int a = 0; a < 2; ++a)
+    for (int q = 0; q < n; ++q) {
+      const uint32_t bit = 1u << (n - 1 - q);
+      switch (str[a][q]) {
+        case 'I': break;
+        case 'X': T[a].xm |= bit; break;
+        case 'Y': T[a].xm |= bit; T[a].zm |= bit; T[a].ny += 1; break;
+        case 'Z': T[a].zm |= bit; break;
+        default: return DVQLS_E_PAULI;
+      }
+    }
+  const PauliOp B = task_observable(n, T[0], T[1], s);
+  *x_mask = B.m;
+  *z_mask = B.z;
+  *phase = B.q;
+  return DVQLS_OK;
+}
 
 int dvqls_launches_per_call(const dvqls_ctx* ctx) {
   if (!ctx) return DVQLS_E_ARG;

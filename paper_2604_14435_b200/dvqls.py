@@ -25,13 +25,15 @@ DVQLS_E_NCCL = -6
 DVQLS_E_UNSUPPORTED = -7
 DVQLS_B_UNIFORM = 0
 DVQLS_B_AMPLITUDES = 1
+DVQLS_MODE_CIRCUITS = 0
+DVQLS_MODE_PAULI = 1
 
 EXPORTED = [
     "dvqls_create", "dvqls_destroy", "dvqls_terms", "dvqls_cost", "dvqls_cost_batch",
     "dvqls_cost_dev", "dvqls_terms_local_dev", "dvqls_last_error", "dvqls_num_circuits",
     "dvqls_local_range", "dvqls_stream", "dvqls_launches_per_call", "dvqls_last_timings",
     "dvqls_nccl_unique_id", "dvqls_build_info", "dvqls_shard_range", "dvqls_state",
-    "dvqls_terms_subset",
+    "dvqls_terms_subset", "dvqls_launch_grid", "dvqls_num_observables", "dvqls_task_observable",
 ]
 
 
@@ -52,7 +54,8 @@ class _BPrep(ctypes.Structure):
 class _Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
                 ("nccl_unique_id", ctypes.c_void_p), ("entangler", ctypes.c_int),
-                ("cuda_stream", ctypes.c_void_p), ("timing", ctypes.c_int), ("max_batch", ctypes.c_int)]
+                ("cuda_stream", ctypes.c_void_p), ("timing", ctypes.c_int), ("max_batch", ctypes.c_int),
+                ("mode", ctypes.c_int)]
 
 
 _lib = None
@@ -87,6 +90,12 @@ def load():
     L.dvqls_stream.argtypes = [vp]
     L.dvqls_stream.restype = vp
     L.dvqls_launches_per_call.argtypes = [vp]
+    L.dvqls_launch_grid.argtypes = [vp]
+    L.dvqls_num_observables.argtypes = [vp]
+    L.dvqls_num_observables.restype = ctypes.c_int64
+    u32p = ctypes.POINTER(ctypes.c_uint32)
+    L.dvqls_task_observable.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, u32p, u32p,
+                                        ctypes.POINTER(ctypes.c_int)]
     L.dvqls_last_timings.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
     L.dvqls_nccl_unique_id.argtypes = [vp]
     L.dvqls_build_info.restype = ctypes.c_char_p
@@ -94,7 +103,7 @@ def load():
                                     ctypes.POINTER(ctypes.c_int64)]
     for name in EXPORTED:
         if name not in ("dvqls_destroy", "dvqls_last_error", "dvqls_num_circuits", "dvqls_stream",
-                        "dvqls_build_info"):
+                        "dvqls_build_info", "dvqls_num_observables"):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -137,7 +146,8 @@ class Context:
     """Owns one dvqls_ctx*.  Methods mirror the C entry points."""
 
     def __init__(self, n, layers, paulis: bytes, coeffs, bkind=DVQLS_B_UNIFORM, b=None, device=-1, rank=0,
-                 world=1, nccl_id: bytes | None = None, entangler=0, stream=None, timing=False, max_batch=16):
+                 world=1, nccl_id: bytes | None = None, entangler=0, stream=None, timing=False, max_batch=16,
+                 mode=0):
         L = load()
         self.n, self.layers = int(n), int(layers)
         self.P = 3 * self.n * self.layers
@@ -161,7 +171,7 @@ class Context:
         if stream is not None:
             sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
         op = _Opts(device, rank, world, ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None,
-                   entangler, sp, 1 if timing else 0, max_batch)
+                   entangler, sp, 1 if timing else 0, max_batch, mode)
         h = ctypes.c_void_p()
         rc = L.dvqls_create(ctypes.byref(h), self.n, self.layers, self.L, paulis, _dp(co), ctypes.byref(bp),
                             ctypes.byref(op))
@@ -226,6 +236,12 @@ class Context:
     def stream_ptr(self) -> int:
         return int(load().dvqls_stream(self.h) or 0)
 
+    def num_observables(self) -> int:
+        return int(load().dvqls_num_observables(self.h))
+
+    def grid(self) -> int:
+        return int(load().dvqls_launch_grid(self.h))
+
     def launches_per_call(self) -> int:
         return int(load().dvqls_launches_per_call(self.h))
 
@@ -272,6 +288,16 @@ def dvqls_cost_batch(ctx: Context, thetas):
 
 def dvqls_destroy(ctx: Context) -> None:
     ctx.destroy()
+
+
+def task_observable(n: int, pauli_l: str, pauli_k: str, s: int):
+    """NEXT-2 host algebra (no device): (x_mask, z_mask, phase) of A_l X_j A_k / A_l A_k."""
+    m, z, q = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_int()
+    rc = load().dvqls_task_observable(n, pauli_l.encode(), pauli_k.encode(), s, ctypes.byref(m), ctypes.byref(z),
+                                      ctypes.byref(q))
+    if rc:
+        raise DvqlsError(rc, "dvqls_task_observable")
+    return int(m.value), int(z.value), int(q.value)
 
 
 def from_workload(w, **opts) -> Context:
