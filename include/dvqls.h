@@ -138,6 +138,21 @@ int dvqls_cost_batch(dvqls_ctx* ctx, int K, const double* thetas, double* out_co
  * Caller synchronises the stream (dvqls_stream) before reading out_dev. */
 int dvqls_cost_dev(dvqls_ctx* ctx, int K, const double* thetas_dev, double* out_dev);
 
+/* NEXT-3: local AND global cost (Eq. 1) of K thetas, device-resident, async.
+ * C_G = 1 - |sum_l c_l beta_l|^2 / Re Psi with beta_l = <b|A_l|x> from the 2L overlap
+ * Hadamard tests (ancilla-controlled V, A_l, U_b^+; Re and Im circuits) and Re Psi the
+ * local cost's denominator sum (global over ranks) of the same call.
+ *   out6_dev  6*K doubles: per theta (C_L, Re E, Im E, Re Psi, Im Psi, C_G); C = NaN when
+ *             Re Psi <= 1e-12
+ *   beta_dev  NULL or 2*L*K doubles: per theta and l, (Re, Im) beta_l */
+int dvqls_costs_dev(dvqls_ctx* ctx, int K, const double* thetas_dev, double* out6_dev, double* beta_dev);
+
+/* Host-buffer variant of dvqls_costs_dev for one theta (synchronous).
+ *   out6      6 doubles (C_L, Re E, Im E, Re Psi, Im Psi, C_G)
+ *   out_beta  NULL or 2*L doubles
+ * Returns DVQLS_E_DEGENERATE if Re Psi <= 1e-12. */
+int dvqls_global_cost(dvqls_ctx* ctx, const double* theta, double* out6, double* out_beta);
+
 /* Device-resident terms of THIS rank's block [c0, c1) for one theta (async).
  *   out_dev  (c1 - c0) doubles in device memory */
 int dvqls_terms_local_dev(dvqls_ctx* ctx, const double* theta_dev, double* out_dev);

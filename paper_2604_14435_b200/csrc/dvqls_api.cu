@@ -25,6 +25,7 @@
 #include "tile.cuh"
 #include "stream.cuh"
 #include "pauli.cuh"
+#include "global.cuh"
 #include "nccl_dl.h"
 
 using namespace dvqls;
@@ -147,6 +148,12 @@ struct dvqls_ctx {
   uint32_t* d_task = nullptr;     // per task: (observable << 2) | q
   double2* d_e = nullptr;         // D expectations of the last terms call
   size_t pauli_smem = 0;
+
+  // NEXT-3 global cost (global.cuh)
+  double2* d_b = nullptr;          // b amplitudes (AMPLITUDES only; uniform b needs none)
+  double* d_beta = nullptr;        // max_batch * L * 2
+  double* d_out6 = nullptr;        // max_batch * 6
+  unsigned* d_gcounter = nullptr;  // last-CTA tickets of overlap_kernel
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   bool timed_once = false;
@@ -330,6 +337,7 @@ void release(dvqls_ctx* c) {
   cudaFree(c->d_tab); cudaFree(c->d_coef); cudaFree(c->d_hv); cudaFree(c->d_theta); cudaFree(c->d_x);
   cudaFree(c->d_terms); cudaFree(c->d_partials); cudaFree(c->d_ep); cudaFree(c->d_out); cudaFree(c->d_gather);
   cudaFree(c->d_obs); cudaFree(c->d_wE); cudaFree(c->d_wP); cudaFree(c->d_task); cudaFree(c->d_e);
+  cudaFree(c->d_b); cudaFree(c->d_beta); cudaFree(c->d_out6); cudaFree(c->d_gcounter);
   cudaFree(c->d_counter); cudaFree(c->d_scratch); cudaFree(c->d_x2); cudaFree(c->d_gates); cudaFree(c->d_cidx); cudaFree(c->d_sub);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
@@ -689,6 +697,10 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
       alloc((void**)&ctx->d_ep, sizeof(double) * KB * 4) || alloc((void**)&ctx->d_out, sizeof(double) * KB * 5) ||
       (ctx->world > 1 && alloc((void**)&ctx->d_gather, sizeof(double) * ctx->world * ctx->chunk)) ||
       alloc((void**)&ctx->d_counter, sizeof(unsigned) * KB) ||
+      alloc((void**)&ctx->d_gcounter, sizeof(unsigned) * KB) ||
+      alloc((void**)&ctx->d_beta, sizeof(double) * 2 * KB * size_t(L)) ||
+      alloc((void**)&ctx->d_out6, sizeof(double) * 6 * KB) ||
+      (ctx->bkind == DVQLS_B_AMPLITUDES && alloc((void**)&ctx->d_b, sizeof(double2) * ctx->N)) ||
       (n > 12 && ctx->mode == DVQLS_MODE_CIRCUITS &&
        alloc((void**)&ctx->d_scratch, sizeof(double2) * size_t(ctx->grid) * ctx->N)) ||
       (ctx->mode == DVQLS_MODE_PAULI &&
@@ -707,7 +719,9 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
     fail(ctx, DVQLS_E_CUDA, "cudaMallocHost failed");
     return bail(DVQLS_E_CUDA);
   }
-  if (cudaMemset(ctx->d_counter, 0, sizeof(unsigned) * KB) ||
+  if (cudaMemset(ctx->d_counter, 0, sizeof(unsigned) * KB) || cudaMemset(ctx->d_gcounter, 0, sizeof(unsigned) * KB) ||
+      (ctx->bkind == DVQLS_B_AMPLITUDES &&
+       cudaMemcpy(ctx->d_b, bprep->amps, sizeof(double2) * ctx->N, cudaMemcpyHostToDevice)) ||
       cudaMemcpy(ctx->d_tab, tab.data(), sizeof(PauliTerm) * L, cudaMemcpyHostToDevice) ||
       cudaMemcpy(ctx->d_coef, coef.data(), sizeof(double2) * L, cudaMemcpyHostToDevice) ||
       (!hv.empty() && cudaMemcpy(ctx->d_hv, hv.data(), sizeof(double2) * ctx->N, cudaMemcpyHostToDevice)) ||
@@ -775,6 +789,36 @@ int dvqls_terms_local_dev(dvqls_ctx* ctx, const double* theta_dev, double* out_d
   if (rc) return rc;
   CK(cudaMemcpyAsync(out_dev, ctx->d_terms, sizeof(double) * (ctx->c1 - ctx->c0), cudaMemcpyDeviceToDevice,
                      ctx->stream));
+  return DVQLS_OK;
+}
+
+int dvqls_costs_dev(dvqls_ctx* ctx, int K, const double* thetas_dev, double* out6_dev, double* beta_dev) {
+  if (!ctx) return DVQLS_E_ARG;
+  ctx->err.clear();
+  if (K < 1 || K > ctx->max_batch) return fail(ctx, DVQLS_E_ARG, "K=%d outside [1, max_batch=%d]", K, ctx->max_batch);
+  if (!thetas_dev || !out6_dev) return fail(ctx, DVQLS_E_ARG, "NULL device pointer");
+  int rc = launch_eval(ctx, K, thetas_dev, true, ctx->d_out);
+  if (rc) return rc;
+  glob::overlap_kernel<<<dim3(ctx->L, K), glob::THREADS, 0, ctx->stream>>>(
+      ctx->d_x, ctx->n, ctx->d_tab, ctx->d_coef, ctx->d_b, ctx->L, ctx->d_out, beta_dev ? beta_dev : ctx->d_beta,
+      out6_dev, ctx->d_gcounter);
+  CK(cudaGetLastError());
+  return DVQLS_OK;
+}
+
+int dvqls_global_cost(dvqls_ctx* ctx, const double* theta, double* out6, double* out_beta) {
+  if (!ctx) return DVQLS_E_ARG;
+  ctx->err.clear();
+  if (!theta || !out6) return fail(ctx, DVQLS_E_ARG, "NULL host pointer");
+  std::memcpy(ctx->h_stage, theta, sizeof(double) * ctx->P);
+  CK(cudaMemcpyAsync(ctx->d_theta, ctx->h_stage, sizeof(double) * ctx->P, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = dvqls_costs_dev(ctx, 1, ctx->d_theta, ctx->d_out6, ctx->d_beta);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(out6, ctx->d_out6, sizeof(double) * 6, cudaMemcpyDeviceToHost, ctx->stream));
+  if (out_beta)
+    CK(cudaMemcpyAsync(out_beta, ctx->d_beta, sizeof(double) * 2 * ctx->L, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (!(out6[3] > 1e-12)) return fail(ctx, DVQLS_E_DEGENERATE, "Re Psi <= 1e-12 (singular A on the ansatz state)");
   return DVQLS_OK;
 }
 

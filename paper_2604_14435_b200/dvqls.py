@@ -34,6 +34,7 @@ EXPORTED = [
     "dvqls_local_range", "dvqls_stream", "dvqls_launches_per_call", "dvqls_last_timings",
     "dvqls_nccl_unique_id", "dvqls_build_info", "dvqls_shard_range", "dvqls_state",
     "dvqls_terms_subset", "dvqls_launch_grid", "dvqls_num_observables", "dvqls_task_observable",
+    "dvqls_costs_dev", "dvqls_global_cost",
 ]
 
 
@@ -91,6 +92,8 @@ def load():
     L.dvqls_stream.restype = vp
     L.dvqls_launches_per_call.argtypes = [vp]
     L.dvqls_launch_grid.argtypes = [vp]
+    L.dvqls_costs_dev.argtypes = [vp, ctypes.c_int, vp, vp, vp]
+    L.dvqls_global_cost.argtypes = [vp, dp, dp, dp]
     L.dvqls_num_observables.argtypes = [vp]
     L.dvqls_num_observables.restype = ctypes.c_int64
     u32p = ctypes.POINTER(ctypes.c_uint32)
@@ -192,6 +195,19 @@ class Context:
         ep = np.empty(4)
         _check(load().dvqls_cost(self.h, _dp(th), _dp(c), _dp(ep)), self.h)
         return (float(c[0]), complex(ep[0], ep[1]), complex(ep[2], ep[3])) if with_E_Psi else float(c[0])
+
+    def global_cost(self, theta, with_beta=False):
+        """NEXT-3: (C_L, C_G, E, Psi[, beta]) of one theta (Eq. 1 and Alg. 1 forms)."""
+        th = self._theta(theta, 1)
+        o = np.empty(6)
+        beta = np.empty(2 * self.L)
+        _check(load().dvqls_global_cost(self.h, _dp(th), _dp(o), _dp(beta)), self.h)
+        res = (float(o[0]), float(o[5]), complex(o[1], o[2]), complex(o[3], o[4]))
+        return res + (beta[0::2] + 1j * beta[1::2],) if with_beta else res
+
+    def costs_dev(self, K, thetas_dev, out6_dev, beta_dev=None):
+        _check(load().dvqls_costs_dev(self.h, int(K), _ptr(thetas_dev), _ptr(out6_dev),
+                                      _ptr(beta_dev) if beta_dev is not None else None), self.h)
 
     def cost_batch(self, thetas):
         th = np.ascontiguousarray(thetas, dtype=np.float64)

@@ -55,7 +55,7 @@ def test_hele_shaw_velocity(dv):
 
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 10])
 def test_random_lcu(dv, n):
-    _check(dv, configs.random_workload(n, 5, 2, seed=300 + n))
+    _check(dv, configs.random_workload(n, min(5, 4 ** n), 2, seed=300 + n))
 
 
 def test_cz_ring(dv):
