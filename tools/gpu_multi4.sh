@@ -1,0 +1,26 @@
+# Multi-GPU pass on one box (run with gpurun --gpus N): NCCL/P2P parity (torchrun), strong scaling
+# of cfg3 at 1..N GPUs with the fused NVLink allreduce and with the NCCL fallback, cfg4 at 1 and N.
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out; TAG=${TAG:-m4}
+NG=$(nvidia-smi -L | wc -l); echo "gpus=$NG" > gpurun_out/${TAG}_info.txt
+nvidia-smi topo -m >> gpurun_out/${TAG}_info.txt 2>&1
+timeout 1200 python -m pytest tests/test_multirank.py -x -q > gpurun_out/${TAG}_pytest.log 2>&1
+P=29600
+for N in 1 2 4 8; do
+  if [ $N -le $NG ]; then
+    P=$((P+1))
+    if [ $N -eq 1 ]; then
+      timeout 600 python bench.py --no-cpu-baseline --no-next2 > gpurun_out/${TAG}_cfg3_n1.json 2> gpurun_out/${TAG}_cfg3_n1.err
+    else
+      timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port $P \
+        bench.py --gpus $N --no-next2 > gpurun_out/${TAG}_cfg3_n$N.json 2> gpurun_out/${TAG}_cfg3_n$N.err
+      P=$((P+1))
+      DVQLS_ALLREDUCE=nccl timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
+        --master-port $P bench.py --gpus $N --no-next2 > gpurun_out/${TAG}_cfg3_n${N}_nccl.json 2> gpurun_out/${TAG}_cfg3_n${N}_nccl.err
+    fi
+  fi
+done
+timeout 600 python bench.py --config cfg4 --no-cpu-baseline --no-next2 --steps 50 > gpurun_out/${TAG}_cfg4_n1.json 2> gpurun_out/${TAG}_cfg4_n1.err
+P=$((P+1))
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 --master-port $P \
+  bench.py --gpus $NG --config cfg4 --no-next2 --steps 50 > gpurun_out/${TAG}_cfg4_n$NG.json 2> gpurun_out/${TAG}_cfg4_n$NG.err
+echo done

@@ -21,6 +21,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--mode", type=int, default=0, help="0 = circuits, 1 = NEXT-2 Pauli fast path")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -34,17 +35,19 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     obj = [dvqls.dvqls_nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    w = {"cfg1": configs.cfg1, "cfg3": configs.cfg3, "cfg2p": configs.cfg2_pressure}[args.config]()
-    ctx = dvqls.from_workload(w, device=local, rank=rank, world=world, nccl_id=obj[0])
+    w = {"cfg1": configs.cfg1, "cfg3": configs.cfg3, "cfg2p": configs.cfg2_pressure,
+         "n12": lambda: configs.random_workload(12, 2, 2, seed=77)}[args.config]()
+    ctx = dvqls.from_workload(w, device=local, rank=rank, world=world, nccl_id=obj[0], mode=args.mode)
     th = w.theta0()
     terms = ctx.terms(th)
     C, E, Psi = ctx.cost(th, with_E_Psi=True)
     ths = np.stack([w.theta0(s) for s in range(3)])
     cb, _ = ctx.cost_batch(ths)
+    CLg, CG, _, _ = ctx.global_cost(th)
     c0, c1 = ctx.local_range()
     ok = True
     # every rank must hold identical global results
-    t = torch.tensor([C, cb[0], cb[1], cb[2], float(terms.sum())], dtype=torch.float64, device="cuda")
+    t = torch.tensor([C, cb[0], cb[1], cb[2], float(terms.sum()), CG], dtype=torch.float64, device="cuda")
     lst = [torch.zeros_like(t) for _ in range(world)]
     dist.all_gather(lst, t)
     if rank == 0:
@@ -55,8 +58,11 @@ def main():
         Cr, Er, Pr = ocost.cost(ref, ocost.coeffs_of(w), w.n, w.L)
         refb = [ocost.cost(sim.workload_terms(w, ths[k]), ocost.coeffs_of(w), w.n, w.L)[0] for k in range(3)]
         same = all(torch.equal(lst[0], x) for x in lst)
-        ok = err <= 1e-10 and abs(C - Cr) <= 1e-10 and max(abs(cb[k] - refb[k]) for k in range(3)) <= 1e-10 and same
-        print(f"world={world} {w.name}: max|term err|={err:.2e} C={C:.12f} oracle={Cr:.12f} "
+        CGr = ocost.global_cost(sim.workload_overlaps(w, th), ocost.coeffs_of(w), Pr)
+        ok = (err <= 1e-10 and abs(C - Cr) <= 1e-10 and max(abs(cb[k] - refb[k]) for k in range(3)) <= 1e-10
+              and same and abs(CG - CGr) <= 1e-10 and abs(CLg - Cr) <= 1e-10)
+        print(f"world={world} mode={args.mode} {w.name}: max|term err|={err:.2e} C={C:.12f} oracle={Cr:.12f} "
+              f"C_G={CG:.12f} oracle={CGr:.12f} "
               f"batch_err={max(abs(cb[k] - refb[k]) for k in range(3)):.2e} ranks_agree={same} "
               f"rank0 block=[{c0},{c1}) -> {'OK' if ok else 'FAIL'}", flush=True)
     flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
