@@ -129,6 +129,9 @@ struct dvqls_ctx {
   char** d_peers = nullptr;
   unsigned long long epoch = 0;
   bool tile_path = false;        // n > 10 (stream.cuh)
+  int team = 0, nteams = 0;      // n >= 15: team mode (stream_team_kernel), T CTAs per circuit
+  double* d_team_acc = nullptr;  // nteams * 2 * team
+  unsigned* d_team_ctr = nullptr;  // nteams barrier counters + 1 error flag
   int tile_bits = 12;            // tile path: amplitudes per SMEM tile = 2^tile_bits
   double2* d_scratch = nullptr;  // grid * N (n > 12)
   double2* d_x2 = nullptr;       // ring ping-pong buffer (n > 12 prefix)
@@ -235,9 +238,21 @@ int launch_pauli(dvqls_ctx* ctx, int K, int64_t d0, int64_t d1, double2* out_e, 
 // (with_cost: 5 doubles C, E, Psi per theta; else 4 doubles E, Psi for the allreduce).
 int launch_hadamard(dvqls_ctx* ctx, int K, int64_t c0, int64_t C, const int64_t* cidx, double* terms, int grid,
                     double* red_out = nullptr, int with_cost = 0) {
+  P2PArgs p2p = make_p2p(ctx, red_out, with_cost);
+  if (ctx->team > 0 && !cidx) {  // team mode: cooperative launch (team barriers need co-residency)
+    int T = ctx->team;
+    unsigned* err = ctx->d_team_ctr + ctx->nteams;
+    void* args[] = {(void*)&ctx->d_x, (void*)&ctx->d_tab, (void*)&ctx->d_coef, (void*)&ctx->L, (void*)&ctx->n,
+                    (void*)&c0, (void*)&C, (void*)&K, (void*)&T, (void*)&ctx->d_scratch, (void*)&terms,
+                    (void*)&ctx->d_partials, (void*)&ctx->d_team_acc, (void*)&ctx->d_team_ctr, (void*)&err,
+                    (void*)&with_cost, (void*)&red_out, (void*)&ctx->d_counter, (void*)&p2p};
+    CK(cudaLaunchCooperativeKernel((const void*)&stream::stream_team_kernel<12>, dim3(ctx->nteams * T),
+                                   dim3(stream::TS<12>::THREADS), args, sizeof(double2) * stream::TS<12>::TN,
+                                   ctx->stream));
+    return DVQLS_OK;
+  }
   if (ctx->tile_path && ctx->n > ctx->tile_bits) grid = std::max(1, grid / K);  // scratch: grid CTAs in total
   dim3 g(grid, K);
-  P2PArgs p2p = make_p2p(ctx, red_out, with_cost);
   if (!ctx->tile_path) {
     void* args[] = {(void*)&ctx->d_x,   (void*)&ctx->d_tab, (void*)&ctx->d_coef,  (void*)&ctx->d_hv,
                     (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&c0, (void*)&C,
@@ -337,6 +352,7 @@ void release(dvqls_ctx* c) {
   cudaFree(c->d_tab); cudaFree(c->d_coef); cudaFree(c->d_hv); cudaFree(c->d_theta); cudaFree(c->d_x);
   cudaFree(c->d_terms); cudaFree(c->d_partials); cudaFree(c->d_ep); cudaFree(c->d_out); cudaFree(c->d_gather);
   cudaFree(c->d_obs); cudaFree(c->d_wE); cudaFree(c->d_wP); cudaFree(c->d_task); cudaFree(c->d_e);
+  cudaFree(c->d_team_acc); cudaFree(c->d_team_ctr);
   cudaFree(c->d_b); cudaFree(c->d_beta); cudaFree(c->d_out6); cudaFree(c->d_gcounter);
   cudaFree(c->d_counter); cudaFree(c->d_scratch); cudaFree(c->d_x2); cudaFree(c->d_gates); cudaFree(c->d_cidx); cudaFree(c->d_sub);
   if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -587,6 +603,29 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   const int64_t need = (Cloc + groups_per_cta - 1) / groups_per_cta;
   ctx->grid = int(std::max<int64_t>(1, std::min(want, need)));
   ctx->NG = int64_t(ctx->grid) * groups_per_cta;
+  if (ctx->tile_path && n >= 15 && ctx->mode == DVQLS_MODE_CIRCUITS && !getenv("DVQLS_NO_TEAM")) {
+    // team mode: T = smallest power of two with (G / T) branches of 2^n x 16 B in <= 80 MB (L2)
+    const void* tf = (const void*)&stream::stream_team_kernel<12>;
+    if (cudaFuncSetAttribute(tf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(sizeof(double2) * stream::TS<12>::TN)) != cudaSuccess) {
+      fail(ctx, DVQLS_E_CUDA, "team kernel smem");
+      return bail(DVQLS_E_CUDA);
+    }
+    int tocc = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, tf, stream::TS<12>::THREADS,
+                                                  sizeof(double2) * stream::TS<12>::TN);
+    const int64_t G = int64_t(prop.multiProcessorCount) * std::max(1, tocc);
+    const double ratio = double(G) * double(ctx->N) * 16.0 / double(size_t(80) << 20);
+    int64_t T = 1;
+    while (T < ratio && T * 2 <= G) T *= 2;
+    T = std::min<int64_t>(T, int64_t(ctx->N >> 12));  // at most one tile per member and pass
+    if (T >= 2) {
+      ctx->team = int(T);
+      ctx->nteams = int(G / T);
+      ctx->grid = ctx->nteams * ctx->team;
+      ctx->NG = std::max<int64_t>(ctx->NG, ctx->nteams);
+    }
+  }
 
   // ---- NEXT-2: symbolic task observables, dedup, folded weights (pauli.cuh) ---------------
   std::vector<pauli::Obs> obs;
@@ -702,7 +741,9 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
       alloc((void**)&ctx->d_out6, sizeof(double) * 6 * KB) ||
       (ctx->bkind == DVQLS_B_AMPLITUDES && alloc((void**)&ctx->d_b, sizeof(double2) * ctx->N)) ||
       (n > 12 && ctx->mode == DVQLS_MODE_CIRCUITS &&
-       alloc((void**)&ctx->d_scratch, sizeof(double2) * size_t(ctx->grid) * ctx->N)) ||
+       alloc((void**)&ctx->d_scratch, sizeof(double2) * size_t(ctx->team ? ctx->nteams : ctx->grid) * ctx->N)) ||
+      (ctx->team && (alloc((void**)&ctx->d_team_acc, sizeof(double) * 2 * size_t(ctx->nteams) * ctx->team) ||
+                     alloc((void**)&ctx->d_team_ctr, sizeof(unsigned) * (size_t(ctx->nteams) + 1)))) ||
       (ctx->mode == DVQLS_MODE_PAULI &&
        (alloc((void**)&ctx->d_obs, sizeof(pauli::Obs) * obs.size()) ||
         alloc((void**)&ctx->d_wE, sizeof(double2) * obs.size()) ||
@@ -720,6 +761,7 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
     return bail(DVQLS_E_CUDA);
   }
   if (cudaMemset(ctx->d_counter, 0, sizeof(unsigned) * KB) || cudaMemset(ctx->d_gcounter, 0, sizeof(unsigned) * KB) ||
+      (ctx->team && cudaMemset(ctx->d_team_ctr, 0, sizeof(unsigned) * (size_t(ctx->nteams) + 1))) ||
       (ctx->bkind == DVQLS_B_AMPLITUDES &&
        cudaMemcpy(ctx->d_b, bprep->amps, sizeof(double2) * ctx->N, cudaMemcpyHostToDevice)) ||
       cudaMemcpy(ctx->d_tab, tab.data(), sizeof(PauliTerm) * L, cudaMemcpyHostToDevice) ||
@@ -926,7 +968,7 @@ int dvqls_terms_subset(dvqls_ctx* ctx, const double* theta, const int64_t* idx, 
                     (void*)&ctx->d_x};
     CK(cudaLaunchKernel(ctx->prefix_fn, dim3(1), dim3(ctx->prefix_threads), args, ctx->prefix_smem, ctx->stream));
   }
-  const int grid = int(std::min<int64_t>(ctx->grid, count));
+  const int grid = int(std::min<int64_t>(ctx->team ? ctx->nteams : ctx->grid, count));  // scratch slots
   int rc = launch_hadamard(ctx, 1, 0, count, ctx->d_cidx, ctx->d_sub, grid);
   if (rc) return rc;
   CK(cudaMemcpyAsync(out, ctx->d_sub, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));

@@ -95,6 +95,17 @@ __device__ __forceinline__ void xchg(double2 (&v)[16], double2* sm, uint32_t t) 
   }
 }
 
+// &base[idx] as one IMAD.WIDE.U32 (idx < 2^28): keeps the per-element address to one
+// instruction instead of a 64-bit add chain
+__device__ __forceinline__ const double2* at(const double2* base, uint32_t idx) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, 16, %2;" : "=l"(r) : "r"(idx), "l"(base));
+  return reinterpret_cast<const double2*>(r);
+}
+__device__ __forceinline__ double2* at(double2* base, uint32_t idx) {
+  return const_cast<double2*>(at(const_cast<const double2*>(base), idx));
+}
+
 // Tile-to-global map of one pass: passengers [0, c), active tile bits at global [b, ...)
 struct Geo {
   int c, b, tb;
@@ -177,7 +188,7 @@ __device__ __forceinline__ void gather(double2 (&v)[16], const double2* __restri
   for (int k = 0; k < 16; ++k) {
     const int r = k ^ (k >> 1);
     jj = cc.step(jj, k);
-    const double2 a = __ldg(x + (jj ^ m));
+    const double2 a = __ldg(at(x, jj ^ m));
     const uint32_t f = smask(w, r);
     v[r] = make_double2(flip(a.x, f), flip(a.y, f));
   }
@@ -195,7 +206,7 @@ __device__ __forceinline__ double readout_t(const double2 (&v)[16], const double
     const int r = k ^ (k >> 1);
     if (k == 8) asm volatile("" ::: "memory");  // at most 8 x loads in flight (register cap)
     jj = cc.step(jj, k);
-    const double2 a = __ldg(x + (jj ^ m));
+    const double2 a = __ldg(at(x, jj ^ m));
     const uint32_t f = smask(w, r);
     const double xr = flip(a.x, f), xi = flip(a.y, f);
     if (k & 1) {
@@ -230,7 +241,7 @@ __device__ __forceinline__ void gload(double2 (&v)[16], const double2* __restric
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     jj = cc.step(jj, k);
-    v[k ^ (k >> 1)] = __ldcg(src + jj);
+    v[k ^ (k >> 1)] = __ldcg(at(src, jj));
   }
 }
 
@@ -240,7 +251,7 @@ __device__ __forceinline__ void gstore(const double2 (&v)[16], double2* __restri
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     jj = cc.step(jj, k);
-    __stcg(dst + jj, v[k ^ (k >> 1)]);
+    __stcg(at(dst, jj), v[k ^ (k >> 1)]);
   }
 }
 
@@ -293,13 +304,15 @@ __device__ __forceinline__ Geo group(int n, int gi, int TB) {
 
 // One pass over the branch of one circuit for group g of a multi-pass (n > TB) circuit.
 // kind: 0 = F1 only, 1 = F1 + Z_j + F2 (middle), 2 = F2 only.
-template <int TB>
-__device__ __forceinline__ void mid_pass(double2* __restrict__ phi, double2* sm, const Geo& g, int kind, int p,
-                                         uint32_t ntiles, uint32_t t) {
-  const int lo = g.c, hi = TB;
-  const bool needLM = lo < 8, needLL = lo < 4;
-  for (uint32_t tau = 0; tau < ntiles; ++tau) {
-    if (tau + 1 < ntiles) prefetch_tile(phi, g, tau + 1, 0u, t, TS<TB>::THREADS);
+// (C = g.c is a template parameter: with constant stage bounds the butterfly code has no
+//  run-time branches, so no register copies at their joins)
+template <int TB, int C>
+__device__ __forceinline__ void mid_pass_c(double2* __restrict__ phi, double2* sm, const Geo& g, int kind, int p,
+                                           uint32_t t0, uint32_t t1, uint32_t t) {
+  constexpr int lo = C, hi = TB;
+  constexpr bool needLM = lo < 8, needLL = lo < 4;
+  for (uint32_t tau = t0; tau < t1; ++tau) {
+    if (tau + 1 < t1) prefetch_tile(phi, g, tau + 1, 0u, t, TS<TB>::THREADS);
     double2 v[16];
     if (!needLM) {  // all active bits in LH: no exchange
       const Cols<TS<TB>::SH> cc(g, t, tau);
@@ -351,6 +364,80 @@ __device__ __forceinline__ void mid_pass(double2* __restrict__ phi, double2* sm,
   }
 }
 
+template <int TB>
+__device__ __forceinline__ void mid_pass(double2* __restrict__ phi, double2* sm, const Geo& g, int kind, int p,
+                                         uint32_t t0, uint32_t t1, uint32_t t) {
+  switch (g.c) {
+    case 2: mid_pass_c<TB, 2>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 3: mid_pass_c<TB, 3>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 4: mid_pass_c<TB, 4>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 5: mid_pass_c<TB, 5>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 6: mid_pass_c<TB, 6>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 7: mid_pass_c<TB, 7>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 8: mid_pass_c<TB, 8>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 9: mid_pass_c<TB, 9>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 10: mid_pass_c<TB, 10>(phi, sm, g, kind, p, t0, t1, t); break;
+    default: mid_pass_c<TB, 11>(phi, sm, g, kind, p, t0, t1, t); break;
+  }
+}
+
+// P0 of a multi-pass numerator circuit on tiles [t0, t1): gather (c-A_k) + F1 on bits 0..TB-1
+template <int TB>
+__device__ __forceinline__ void first_pass(double2* __restrict__ phi, const double2* __restrict__ x, double2* sm,
+                                           const Geo& g0, const PauliTerm& Tk, bool big_x, uint32_t t0, uint32_t t1,
+                                           uint32_t t) {
+  constexpr int SH = TS<TB>::SH;
+  for (uint32_t tau = t0; tau < t1; ++tau) {
+    if (big_x && tau + 1 < t1) prefetch_tile(x, g0, tau + 1, Tk.xm & ~uint32_t(TS<TB>::TN - 1), t, TS<TB>::THREADS);
+    double2 v[16];
+    gather(v, x, Cols<LM_>(g0, t, tau), Tk.xm, Tk.zm);
+    stages<LM_, TB>(v, 0, TB);
+    xchg<LM_, LL_>(v, sm, t);
+    stages<LL_, TB>(v, 0, TB);
+    xchg<LL_, SH>(v, sm, t);
+    stages<SH, TB>(v, 0, TB);
+    gstore(v, phi, Cols<SH>(g0, t, tau));
+  }
+}
+
+// last pass on tiles [t0, t1): F2 on bits 0..TB-1 + readout (c-A_l); returns this thread's sum
+template <int TB>
+__device__ __forceinline__ double last_pass(const double2* __restrict__ phi, const double2* __restrict__ x,
+                                            double2* sm, const Geo& g0, const PauliTerm& Tl, bool im, bool big_x,
+                                            uint32_t t0, uint32_t t1, uint32_t t) {
+  constexpr int SH = TS<TB>::SH;
+  double acc = 0.0;
+  for (uint32_t tau = t0; tau < t1; ++tau) {
+    if (tau + 1 < t1) {
+      prefetch_tile(phi, g0, tau + 1, 0u, t, TS<TB>::THREADS);
+      if (big_x) prefetch_tile(x, g0, tau + 1, Tl.xm & ~uint32_t(TS<TB>::TN - 1), t, TS<TB>::THREADS);
+    }
+    double2 v[16];
+    gload(v, phi, Cols<SH>(g0, t, tau));
+    stages<SH, TB>(v, 0, TB);
+    xchg<SH, LL_>(v, sm, t);
+    stages<LL_, TB>(v, 0, TB);
+    xchg<LL_, LM_>(v, sm, t);
+    stages<LM_, TB>(v, 0, TB);
+    acc += readout(v, x, Cols<LM_>(g0, t, tau), Tl.xm, Tl.zm, im);
+  }
+  return acc;
+}
+
+// denominator circuit on tiles [t0, t1): sum_j conj(sgn_l(j) x_{j^m_l}) sgn_k(j^m_k) x_{j^m_k}
+template <int TB>
+__device__ __forceinline__ double den_pass(const double2* __restrict__ x, const Geo& g0, const PauliTerm& Tk,
+                                           const PauliTerm& Tl, bool im, uint32_t t0, uint32_t t1, uint32_t t) {
+  double acc = 0.0;
+  for (uint32_t tau = t0; tau < t1; ++tau) {
+    const Cols<LM_> cm(g0, t, tau);
+    double2 v[16];
+    gather(v, x, cm, Tk.xm, Tk.zm);
+    acc += readout(v, x, cm, Tl.xm, Tl.zm, im);
+  }
+  return acc;
+}
+
 template <int TB, bool HH>
 __global__ void __launch_bounds__(TS<TB>::THREADS, 2)
 stream_hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ tab,
@@ -390,12 +477,7 @@ stream_hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __res
     double acc = 0.0;
     if (sidx == 0) {
       // ---- denominator: <x| A_l A_k |x> term, straight from x
-      for (uint32_t tau = 0; tau < ntiles; ++tau) {
-        const Cols<LM_> cm(g0, t, tau);
-        double2 v[16];
-        gather(v, x, cm, Tk.xm, Tk.zm);
-        acc += readout(v, x, cm, Tl.xm, Tl.zm, im);
-      }
+      acc = den_pass<TB>(x, g0, Tk, Tl, im, 0, ntiles, t);
     } else if (n <= TB) {
       // ---- one tile: the whole numerator circuit on chip
       const int p = n - 1 - (sidx - 1);  // Z_j bit position, j = s - 1
@@ -407,60 +489,35 @@ stream_hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __res
         zsign(v, cm, p);
         householder(v, hv, cm, hv_scale, red, bc, T::THREADS);
       } else {
-        stages<LM_, TB>(v, 0, n);
+        stages<LM_, TB>(v, 0, TB);
         xchg<LM_, LL_>(v, sm, t);
-        stages<LL_, TB>(v, 0, n);
+        stages<LL_, TB>(v, 0, TB);
         xchg<LL_, SH>(v, sm, t);
-        stages<SH, TB>(v, 0, n);
+        stages<SH, TB>(v, 0, TB);
         zsign(v, Cols<SH>(g0, t, 0), p);
-        stages<SH, TB>(v, 0, n);
+        stages<SH, TB>(v, 0, TB);
         xchg<SH, LL_>(v, sm, t);
-        stages<LL_, TB>(v, 0, n);
+        stages<LL_, TB>(v, 0, TB);
         xchg<LL_, LM_>(v, sm, t);
-        stages<LM_, TB>(v, 0, n);
+        stages<LM_, TB>(v, 0, TB);
       }
       acc = readout(v, x, cm, Tl.xm, Tl.zm, im);
     } else {
       // ---- multi-pass numerator circuit through the CTA's scratch
       const int p = n - 1 - (sidx - 1);
-      // P0: gather + F1 on g0 (bits 0..TB-1), store in LH
-      for (uint32_t tau = 0; tau < ntiles; ++tau) {
-        if (big_x && tau + 1 < ntiles) prefetch_tile(x, g0, tau + 1, Tk.xm & ~uint32_t(T::TN - 1), t, T::THREADS);
-        double2 v[16];
-        gather(v, x, Cols<LM_>(g0, t, tau), Tk.xm, Tk.zm);
-        stages<LM_, TB>(v, 0, TB);
-        xchg<LM_, LL_>(v, sm, t);
-        stages<LL_, TB>(v, 0, TB);
-        xchg<LL_, SH>(v, sm, t);
-        stages<SH, TB>(v, 0, TB);
-        gstore(v, phi, Cols<SH>(g0, t, tau));
-      }
+      first_pass<TB>(phi, x, sm, g0, Tk, big_x, 0, ntiles, t);
       __syncthreads();
       if (ng == 2) {
-        mid_pass<TB>(phi, sm, group(n, 1, TB), 1, p, ntiles, t);
+        mid_pass<TB>(phi, sm, group(n, 1, TB), 1, p, 0, ntiles, t);
       } else {
-        mid_pass<TB>(phi, sm, group(n, 1, TB), 0, p, ntiles, t);
+        mid_pass<TB>(phi, sm, group(n, 1, TB), 0, p, 0, ntiles, t);
         __syncthreads();
-        mid_pass<TB>(phi, sm, group(n, 2, TB), 1, p, ntiles, t);
+        mid_pass<TB>(phi, sm, group(n, 2, TB), 1, p, 0, ntiles, t);
         __syncthreads();
-        mid_pass<TB>(phi, sm, group(n, 1, TB), 2, p, ntiles, t);
+        mid_pass<TB>(phi, sm, group(n, 1, TB), 2, p, 0, ntiles, t);
       }
       __syncthreads();
-      // last pass: F2 on g0 + readout
-      for (uint32_t tau = 0; tau < ntiles; ++tau) {
-        if (tau + 1 < ntiles) {
-          prefetch_tile(phi, g0, tau + 1, 0u, t, T::THREADS);
-          if (big_x) prefetch_tile(x, g0, tau + 1, Tl.xm & ~uint32_t(T::TN - 1), t, T::THREADS);
-        }
-        double2 v[16];
-        gload(v, phi, Cols<SH>(g0, t, tau));
-        stages<SH, TB>(v, 0, TB);
-        xchg<SH, LL_>(v, sm, t);
-        stages<LL_, TB>(v, 0, TB);
-        xchg<LL_, LM_>(v, sm, t);
-        stages<LM_, TB>(v, 0, TB);
-        acc += readout(v, x, Cols<LM_>(g0, t, tau), Tl.xm, Tl.zm, im);
-      }
+      acc = last_pass<TB>(phi, x, sm, g0, Tl, im, big_x, 0, ntiles, t);
       __syncthreads();  // scratch reads of this circuit done before the next circuit's P0
     }
     double val = block_sum(acc, red, T::THREADS);
@@ -480,6 +537,196 @@ stream_hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __res
     o[0] = acc4[0]; o[1] = acc4[1]; o[2] = acc4[2]; o[3] = acc4[3];
   }
   if (red_out) finish_partials(partials, G, kth, n, with_cost, red_out, counter, p2p.world > 1 ? &p2p : nullptr);
+}
+
+}  // namespace stream
+}  // namespace dvqls
+
+namespace dvqls {
+namespace stream {
+
+// ---------------------------------------------------------------------------------------------
+// Team mode (n >= 15): T co-resident CTAs (cooperative launch) share ONE circuit at a time, each
+// taking a contiguous 1/T of the tiles of every pass, with a team barrier between passes.  Only
+// NT = grid / T branches are in flight, NT * 2^n * 16 B <= ~80 MB, so the scratch traffic of the
+// three passes stays in L2 instead of HBM (the per-CTA kernel above keeps 296 branches in flight:
+// 1.2 GB at n = 18).  Every circuit is still simulated on its own; the T partial readout sums
+// are combined in a fixed order, so results are deterministic for a launch configuration.
+// ---------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Barrier of the T CTAs of a team on a monotone counter (target = T * barriers so far).
+// A bounded spin (~10 s at 2 GHz) sets *err and releases every waiter instead of hanging.
+__device__ __forceinline__ void team_sync(unsigned* ctr, unsigned target, unsigned* err) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    const long long t0 = clock64();
+    while (int(ld_acquire(ctr) - target) < 0) {
+      if (ld_acquire(err)) break;
+      if (clock64() - t0 > 20000000000ll) { atomicExch(err, 1u); break; }
+      __nanosleep(40);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// cost units of circuits [0, c) of one theta in canonical order: denominator 1, numerator WN
+constexpr int64_t WN = 4;
+__device__ __forceinline__ int64_t cum_cost(int64_t c, int n) {
+  const int64_t P = 2 * int64_t(n + 1), per = 2 + 2 * int64_t(n) * WN;
+  const int64_t q = c / P, r = c % P;
+  return q * per + (r < 2 ? r : 2) + (r > 2 ? (r - 2) * WN : 0);
+}
+// flattened work f in [0, K*Cloc): theta f / Cloc, circuit c0 + f % Cloc
+__device__ __forceinline__ int64_t cum_flat(int64_t f, int64_t c0, int64_t Cloc, int n) {
+  const int64_t th = f / Cloc, base = cum_cost(c0, n);
+  return th * (cum_cost(c0 + Cloc, n) - base) + cum_cost(c0 + f % Cloc, n) - base;
+}
+// smallest f in [0, W] with cum_flat(f) >= target
+__device__ __forceinline__ int64_t split_flat(int64_t target, int64_t W, int64_t c0, int64_t Cloc, int n) {
+  int64_t lo = 0, hi = W;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (cum_flat(mid, c0, Cloc, n) >= target) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+template <int TB>
+__global__ void __launch_bounds__(TS<TB>::THREADS, 2)
+stream_team_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ tab,
+                   const double2* __restrict__ coef, int L, int n, int64_t c0, int64_t Cloc, int K, int T,
+                   double2* __restrict__ scratch, double* __restrict__ out_terms, double* __restrict__ partials,
+                   double* __restrict__ team_acc, unsigned* __restrict__ team_ctr, unsigned* __restrict__ err,
+                   int with_cost, double* __restrict__ red_out, unsigned* __restrict__ counter, P2PArgs p2p) {
+  using TT = TS<TB>;
+  double2* sm = dvqls_smem;
+  __shared__ double red[TT::THREADS / 32];
+  __shared__ double acc4[4];
+  const int NT = gridDim.x / T;
+  const int g = blockIdx.x / T, r = blockIdx.x % T;
+  const uint32_t N = 1u << n;
+  const uint32_t t = threadIdx.x;
+  const int ng = ngroups(n, TB);
+  const uint32_t ntiles = N >> TB;
+  const uint32_t ta = uint32_t(uint64_t(r) * ntiles / T), tb = uint32_t(uint64_t(r + 1) * ntiles / T);
+  const Geo g0 = group(n, 0, TB);
+  const bool big_x = n > 22;
+  double2* __restrict__ phi = scratch + size_t(g) * N;
+  unsigned* ctr = team_ctr + g;
+  unsigned bars = 0;
+  const bool lead = r == 0 && t == 0;
+
+  // weighted contiguous split of the flattened (theta, circuit) work over the teams
+  const int64_t W = int64_t(K) * Cloc;
+  const int64_t total = cum_flat(W, c0, Cloc, n);
+  const int64_t fb = split_flat(total * g / NT, W, c0, Cloc, n);
+  const int64_t fe = split_flat(total * (g + 1) / NT, W, c0, Cloc, n);
+  if (lead)
+    for (int k = 0; k < K; ++k)
+      for (int q = 0; q < 4; ++q) partials[(size_t(k) * NT + g) * 4 + q] = 0.0;
+  if (t == 0) acc4[0] = acc4[1] = acc4[2] = acc4[3] = 0.0;
+  int cur = -1;
+  int parity = 0;
+  for (int64_t f = fb; f < fe; ++f) {
+    const int th = int(f / Cloc);
+    const int64_t cl = f % Cloc, c = c0 + cl;
+    if (th != cur) {
+      if (lead && cur >= 0)
+        for (int q = 0; q < 4; ++q) partials[(size_t(cur) * NT + g) * 4 + q] = acc4[q];
+      if (t == 0) acc4[0] = acc4[1] = acc4[2] = acc4[3] = 0.0;
+      cur = th;
+    }
+    const double2* __restrict__ x = x_all + size_t(th) * N;
+    const int64_t tk = c >> 1;
+    const int part = int(c & 1);
+    const int sidx = int(tk % (n + 1));
+    const int64_t lk = tk / (n + 1);
+    const int k = int(lk % L), l = int(lk / L);
+    const PauliTerm Tk = tab[k], Tl = tab[l];
+    const int q = (Tk.ny + Tl.ny + 3 * part) & 3;
+    const bool im = q & 1;
+    double acc;
+    if (sidx == 0) {
+      acc = den_pass<TB>(x, g0, Tk, Tl, im, ta, tb, t);
+    } else {
+      const int p = n - 1 - (sidx - 1);
+      first_pass<TB>(phi, x, sm, g0, Tk, big_x, ta, tb, t);
+      team_sync(ctr, unsigned(T) * ++bars, err);
+      if (ng == 2) {
+        mid_pass<TB>(phi, sm, group(n, 1, TB), 1, p, ta, tb, t);
+      } else {
+        mid_pass<TB>(phi, sm, group(n, 1, TB), 0, p, ta, tb, t);
+        team_sync(ctr, unsigned(T) * ++bars, err);
+        mid_pass<TB>(phi, sm, group(n, 2, TB), 1, p, ta, tb, t);
+        team_sync(ctr, unsigned(T) * ++bars, err);
+        mid_pass<TB>(phi, sm, group(n, 1, TB), 2, p, ta, tb, t);
+      }
+      team_sync(ctr, unsigned(T) * ++bars, err);
+      acc = last_pass<TB>(phi, x, sm, g0, Tl, im, big_x, ta, tb, t);
+    }
+    const double part_sum = block_sum(acc, red, TT::THREADS);
+    double* slot = team_acc + (size_t(g) * 2 + parity) * T;
+    if (t == 0) slot[r] = part_sum;
+    // all members' sums visible; the scratch is free for the next circuit's P0
+    team_sync(ctr, unsigned(T) * ++bars, err);
+    if (lead) {
+      double val = 0.0;
+      for (int m = 0; m < T; ++m) val += __ldcg(slot + m);  // fixed member order
+      if (sidx > 0) val *= 1.0 / double(N);
+      val = (q == 1 || q == 2) ? -val : val;
+      if (ld_acquire(err)) val = __longlong_as_double(0x7ff8000000000000ll);
+      out_terms[size_t(th) * Cloc + cl] = val;
+      const double2 cl_ = coef[l], ck = coef[k];
+      const double wr = cl_.x * ck.x + cl_.y * ck.y, wi = cl_.x * ck.y - cl_.y * ck.x;
+      const double cr = part == 0 ? wr * val : -wi * val;
+      const double ci = part == 0 ? wi * val : wr * val;
+      if (sidx == 0) { acc4[2] += cr; acc4[3] += ci; } else { acc4[0] += cr; acc4[1] += ci; }
+    }
+    parity ^= 1;
+  }
+  if (lead && cur >= 0)
+    for (int q = 0; q < 4; ++q) partials[(size_t(cur) * NT + g) * 4 + q] = acc4[q];
+
+  // ---- a9/a10: the last CTA of the grid sums every theta's NT partials in a fixed order ----
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (t == 0) {
+    const bool bad = ld_acquire(err) != 0;
+    for (int kk = 0; kk < K && red_out; ++kk) {
+      double e0 = 0, e1 = 0, e2 = 0, e3 = 0;
+      for (int gg = 0; gg < NT; ++gg) {
+        const double* pp = partials + (size_t(kk) * NT + gg) * 4;
+        e0 += __ldcg(pp + 0); e1 += __ldcg(pp + 1); e2 += __ldcg(pp + 2); e3 += __ldcg(pp + 3);
+      }
+      if (bad) e2 = __longlong_as_double(0x7ff8000000000000ll);
+      if (p2p.world > 1) {
+        p2p_allreduce(p2p, kk, n, e0, e1, e2, e3, red_out);
+      } else if (with_cost) {
+        double* o = red_out + size_t(kk) * 5;
+        o[0] = cost_of_dev(e0, e2, n); o[1] = e0; o[2] = e1; o[3] = e2; o[4] = e3;
+      } else {
+        double* o = red_out + size_t(kk) * 4;
+        o[0] = e0; o[1] = e1; o[2] = e2; o[3] = e3;
+      }
+    }
+    for (int gg = 0; gg < NT; ++gg) team_ctr[gg] = 0u;  // ready for the next launch
+    *err = 0u;
+    *counter = 0u;
+  }
 }
 
 }  // namespace stream
