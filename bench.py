@@ -429,6 +429,32 @@ def main():
     barrier()
     e2e_s = max_over_ranks(e2e_s)
 
+    # ---- NEXT-3 global cost: C_L and C_G of the same call (dvqls_costs_dev) ----------------------
+    next3 = None
+    if not args.no_next2:
+        out6 = torch.empty(6 * KT, dtype=torch.float64, device=dev)
+        g_steps = max(3, args.steps // 4)
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                flush.zero_()
+                ctx.costs_dev(KT, th_dev, out6)
+            barrier()
+            gs = [torch.cuda.Event(enable_timing=True) for _ in range(g_steps)]
+            ge = [torch.cuda.Event(enable_timing=True) for _ in range(g_steps)]
+            for i in range(g_steps):
+                flush.zero_()
+                gs[i].record(stream)
+                ctx.costs_dev(KT, th_dev, out6)
+                ge[i].record(stream)
+            barrier()
+        g_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in zip(gs, ge)))
+        o6 = out6.view(KT, 6).cpu().numpy()
+        next3 = {"evals_per_s": KT * g_steps / (g_ms * 1e-3), "ms_per_step": g_ms / g_steps,
+                 "overhead_vs_local_only": (g_ms / g_steps) / (dev_ms / args.steps) - 1.0,
+                 "C_G_theta0": float(o6[0, 5]), "C_L_theta0": float(o6[0, 0]),
+                 "sandwich_ok": bool(np.all((o6[:, 0] <= o6[:, 5] + 1e-12) & (o6[:, 5] <= w.n * o6[:, 0] + 1e-12))),
+                 "note": "NEXT-3: local cost path + 2L overlap Hadamard tests -> C_G (Eq. 1) in the same call"}
+
     # ---- NEXT-2 algebraic fast path (flagged; reported separately, never the headline) ----------
     next2 = None
     if w.bkind == 0 and not args.no_next2:
@@ -531,6 +557,7 @@ def main():
             "cost": float(res[0, 0]),
             "cost_k1": float(res1[0]),
             "next2_pauli": next2,
+            "next3_global": next3,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(w, thetas[0])

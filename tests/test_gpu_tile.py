@@ -77,3 +77,39 @@ def test_parameter_shift_pair_cost(dv):
         ref = sim.workload_terms(w, pair[k], idx=idx)
         Cr = ocost.cost(ref, ocost.coeffs_of(w), w.n, w.L)[0]
         assert abs(cb[k] - Cr) <= TOL
+
+
+@pytest.mark.parametrize("n,ent", [(15, 0), (16, 1), (17, 0)])
+def test_team_mode_full(dv, n, ent):
+    """n >= 15 runs the team kernel (T CTAs per circuit, cooperative launch): full terms, cost and a
+    batch of 3 thetas against the oracle."""
+    w = configs.random_workload(n, 2, 2, seed=70 + n, entangler=ent)
+    ctx = dv.from_workload(w, max_batch=4)
+    try:
+        th = w.theta0()
+        g = ctx.terms(th)
+        C = ctx.cost(th)
+        ths = np.stack([w.theta0(s) for s in range(3)])
+        cb, _ = ctx.cost_batch(ths)
+    finally:
+        ctx.destroy()
+    ref = sim.workload_terms(w, th)
+    assert np.max(np.abs(g - ref)) <= TOL
+    assert abs(C - ocost.cost(ref, ocost.coeffs_of(w), w.n, w.L)[0]) <= TOL
+    for k in range(3):
+        rk = sim.workload_terms(w, ths[k])
+        assert abs(cb[k] - ocost.cost(rk, ocost.coeffs_of(w), w.n, w.L)[0]) <= TOL
+
+
+def test_team_mode_cfg5_n16_sampled(dv):
+    """Config 5 at n = 16 through the team kernel (all 139,264 circuits), strided sample vs oracle."""
+    w = configs.cfg5(16)
+    th = w.theta0()
+    ctx = dv.from_workload(w)
+    try:
+        g = ctx.terms(th)
+    finally:
+        ctx.destroy()
+    idx = np.linspace(0, w.n_circuits - 1, 24).astype(np.int64)
+    idx[1::2] |= 1
+    assert np.max(np.abs(g[idx] - sim.workload_terms(w, th, idx=idx))) <= TOL

@@ -72,15 +72,15 @@ def test_gloo_sharded_reduction_equals_single_process(world):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("config", ["cfg1", "cfg2p", "cfg3"])
-def test_nccl_multigpu(config):
+@pytest.mark.parametrize("config,mode", [("cfg1", 0), ("cfg2p", 0), ("cfg3", 0), ("n12", 0), ("cfg1", 1), ("cfg3", 1)])
+def test_nccl_multigpu(config, mode):
     import torch
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--master-addr", "127.0.0.1",
            "--master-port", str(_free_port()), "--nproc-per-node", str(min(n, 8)),
-           os.path.join(ROOT, "tools", "multirank_check.py"), "--config", config]
+           os.path.join(ROOT, "tools", "multirank_check.py"), "--config", config, "--mode", str(mode)]
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
