@@ -455,6 +455,24 @@ def main():
                  "sandwich_ok": bool(np.all((o6[:, 0] <= o6[:, 5] + 1e-12) & (o6[:, 5] <= w.n * o6[:, 0] + 1e-12))),
                  "note": "NEXT-3: local cost path + 2L overlap Hadamard tests -> C_G (Eq. 1) in the same call"}
 
+    # ---- NEXT-4 GPU Pauli decomposition + pruning of a dense A (rank 0, side measurement) -------
+    next4 = None
+    if rank == 0 and not args.no_next2:
+        from dvqls_inputs import problems
+        nd = 12
+        A, _ = problems.tridiag_toeplitz(nd, 2.0, -1.0, -1.0)
+        best = None
+        for _ in range(3):
+            terms, nrm, ms = dvqls.decompose(A, 0.01, device=local, timing=True)
+            best = ms if best is None else min(best, ms)
+        byts = 48 * 4 ** nd
+        pk = float(load_peaks()[0]["hbm_gbs"])
+        next4 = {"n": nd, "terms": len(terms), "ms": best, "GBps": byts / (best * 1e-3) / 1e9,
+                 "hbm_frac": byts / (best * 1e-3) / 1e9 / pk,
+                 "note": ("NEXT-4: 4^n coefficients by per-x-mask FWHT + pruning + sort on the GPU; algorithmic "
+                          "bytes 48*4^n (A read, C written and read) over the device time (best of 3)")}
+        del A
+
     # ---- NEXT-2 algebraic fast path (flagged; reported separately, never the headline) ----------
     next2 = None
     if w.bkind == 0 and not args.no_next2:
@@ -558,6 +576,7 @@ def main():
             "cost_k1": float(res1[0]),
             "next2_pauli": next2,
             "next3_global": next3,
+            "next4_decompose": next4,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(w, thetas[0])

@@ -169,6 +169,30 @@ int dvqls_state(dvqls_ctx* ctx, const double* theta, double* out_state);
  *   out   count doubles, out[i] = <Z_anc> of circuit idx[i] */
 int dvqls_terms_subset(dvqls_ctx* ctx, const double* theta, const int64_t* idx, int64_t count, double* out);
 
+/* ---- NEXT-4: Pauli decomposition + pruning on the GPU (no context) ------
+ * Alg. 1 Steps 1-2 (FWHT-based decomposition P:379, pruning below 1 % of the l2
+ * norm P:490):  c_P = tr(P A)/2^n for all 4^n Pauli strings P, then keep |c| >= 1e-14 and
+ * |c| >= eps * ||c||_2 (inclusive), ordered by descending |c| (magnitudes within
+ * 1e-12 * ||c||_2 tie) then lexicographically with I < X < Y < Z (SURVEY §8(c) reading 15).
+ *   n            1..13 (A is 2^n x 2^n; 1 GB of complex128 at n = 13)
+ *   A            2^n * 2^n complex, row-major, interleaved (re, im), HOST memory (copied)
+ *   eps          0 <= eps < 1
+ *   max_terms    capacity of out_paulis (max_terms*n chars) and out_coeffs (2*max_terms doubles)
+ *   out_L        number of surviving terms (set even when it exceeds max_terms: DVQLS_E_ARG)
+ *   out_norm     NULL or ||c||_2
+ *   device       CUDA device ordinal, -1 = current
+ *   out_ms       NULL or device milliseconds of transform + pruning + sort (CUDA events,
+ *                after the host-to-device copy of A)
+ * The output feeds dvqls_create (pauli_terms, coeffs) directly.  Synchronous; allocates its
+ * own device buffers (2 x 16 * 4^n bytes).  More than 4096 survivors: DVQLS_E_UNSUPPORTED.
+ * Errors: dvqls_decompose_error(). */
+int dvqls_decompose(int n, const double* A, double eps, int64_t max_terms, char* out_paulis,
+                    double* out_coeffs, int64_t* out_L, double* out_norm, int device, float* out_ms);
+/* All 4^n coefficients, out_coeffs[2 * (m * 2^n + z) + {0,1}] = c_{P(m, z)} with x-mask m and
+ * z-mask z (big-endian bits; character q <-> bit n-1-q), same transform as dvqls_decompose. */
+int dvqls_pauli_coefficients(int n, const double* A, double* out_coeffs, int device);
+const char* dvqls_decompose_error(void);
+
 /* ---- introspection ------------------------------------------------------ */
 const char* dvqls_last_error(const dvqls_ctx* ctx); /* "" if none; static text if ctx NULL */
 int64_t dvqls_num_circuits(const dvqls_ctx* ctx);   /* 2(n+1)L^2 */

@@ -94,3 +94,18 @@ def decompose_pruned(A: np.ndarray, eps: float):
     q = 1e-12 * norm
     out.sort(key=lambda t: (-int(round(abs(t[0]) / q)), lex_code(t[1], t[2], n)))
     return [(complex(c), pauli_string(m, z, n)) for c, m, z in out], norm
+
+
+def coefficient(A: np.ndarray, m: int, z: int) -> complex:
+    """One coefficient by the same definition, O(2^n): i^{popcount(m & z)} / 2^n *
+    sum_k (-1)^{popcount(k & z)} A[k, k ^ m] (for sampled checks at sizes where the full
+    4^n transform by matmul is too slow)."""
+    A = np.asarray(A)
+    N = A.shape[0]
+    k = np.arange(N)
+    kz = k & z
+    par = np.zeros(N, dtype=np.int64)
+    for b in range(N.bit_length() - 1):
+        par ^= (kz >> b) & 1
+    s = np.sum(np.where(par == 1, -1.0, 1.0) * A[k, k ^ m])
+    return complex((1j) ** (bin(m & z).count("1") % 4) * s / N)

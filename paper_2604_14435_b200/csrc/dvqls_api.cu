@@ -26,6 +26,7 @@
 #include "stream.cuh"
 #include "pauli.cuh"
 #include "global.cuh"
+#include "decomp.cuh"
 #include "nccl_dl.h"
 
 using namespace dvqls;
@@ -603,7 +604,10 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   const int64_t need = (Cloc + groups_per_cta - 1) / groups_per_cta;
   ctx->grid = int(std::max<int64_t>(1, std::min(want, need)));
   ctx->NG = int64_t(ctx->grid) * groups_per_cta;
-  if (ctx->tile_path && n >= 15 && ctx->mode == DVQLS_MODE_CIRCUITS && !getenv("DVQLS_NO_TEAM")) {
+  // Team mode is opt-in (DVQLS_TEAM=1): measured on B200 it cuts DRAM reads ~10x but the team
+  // barriers cost as much as they save (cfg5 n=16: 210 vs 217 ms, n=18: 1218 vs 1123 ms, K=2).
+  if (ctx->tile_path && n >= 15 && ctx->mode == DVQLS_MODE_CIRCUITS && getenv("DVQLS_TEAM") &&
+      atoi(getenv("DVQLS_TEAM")) == 1) {
     // team mode: T = smallest power of two with (G / T) branches of 2^n x 16 B in <= 80 MB (L2)
     const void* tf = (const void*)&stream::stream_team_kernel<12>;
     if (cudaFuncSetAttribute(tf, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -615,7 +619,9 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, tf, stream::TS<12>::THREADS,
                                                   sizeof(double2) * stream::TS<12>::TN);
     const int64_t G = int64_t(prop.multiProcessorCount) * std::max(1, tocc);
-    const double ratio = double(G) * double(ctx->N) * 16.0 / double(size_t(80) << 20);
+    const char* mb = getenv("DVQLS_TEAM_L2_MB");  // tuning knob: L2 budget of the in-flight branches
+    const double budget = double(size_t(mb && atoi(mb) > 0 ? atoi(mb) : 80) << 20);
+    const double ratio = double(G) * double(ctx->N) * 16.0 / budget;
     int64_t T = 1;
     while (T < ratio && T * 2 <= G) T *= 2;
     T = std::min<int64_t>(T, int64_t(ctx->N >> 12));  // at most one tile per member and pass
@@ -975,6 +981,116 @@ int dvqls_terms_subset(dvqls_ctx* ctx, const double* theta, const int64_t* idx, 
   CK(cudaStreamSynchronize(ctx->stream));
   return DVQLS_OK;
 }
+
+// ---- NEXT-4: Pauli decomposition + pruning (decomp.cuh) ---------------------------------------
+namespace {
+struct DecompBufs {
+  double2* A = nullptr;
+  double2* C = nullptr;
+  double* sq = nullptr;
+  double* norm = nullptr;
+  unsigned long long* count = nullptr;
+  uint64_t* idx = nullptr;
+  double2* oc = nullptr;
+  char* os = nullptr;
+  cudaStream_t st = nullptr;
+  ~DecompBufs() {
+    cudaFree(A); cudaFree(C); cudaFree(sq); cudaFree(norm); cudaFree(count); cudaFree(idx); cudaFree(oc); cudaFree(os);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+thread_local std::string g_decomp_err;
+
+int decomp_fail(int code, const char* msg) {
+  g_decomp_err = msg;
+  return code;
+}
+
+// steps 1 (+ norm) of NEXT-4 on the device: C[m, z] and ||c||_2
+int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, cudaEvent_t* ev0 = nullptr) {
+  if (device >= 0 && cudaSetDevice(device) != cudaSuccess) return decomp_fail(DVQLS_E_CUDA, "cudaSetDevice");
+  int dev = 0;
+  cudaDeviceProp prop;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10)
+    return decomp_fail(DVQLS_E_CUDA, "libdvqls is built for sm_100a only");
+  const size_t N = size_t(1) << n, NN = N * N;
+  if (cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking) || cudaMalloc((void**)&b.A, sizeof(double2) * NN) ||
+      cudaMalloc((void**)&b.C, sizeof(double2) * NN) || cudaMalloc((void**)&b.sq, sizeof(double) * N) ||
+      cudaMalloc((void**)&b.norm, sizeof(double)) || cudaMalloc((void**)&b.count, sizeof(unsigned long long)))
+    return decomp_fail(DVQLS_E_CUDA, "cudaMalloc failed (decomposition)");
+  if (cudaMemcpyAsync(b.A, A_host, sizeof(double2) * NN, cudaMemcpyHostToDevice, b.st))
+    return decomp_fail(DVQLS_E_CUDA, "copy of A failed");
+  const size_t smem = sizeof(double2) * N;
+  if (cudaFuncSetAttribute((const void*)&decomp::fwht_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(smem)))
+    return decomp_fail(DVQLS_E_CUDA, "fwht_rows_kernel smem");
+  if (ev0 && (cudaEventCreate(ev0) || cudaEventRecord(*ev0, b.st))) return decomp_fail(DVQLS_E_CUDA, "event");
+  decomp::fwht_rows_kernel<<<unsigned(N), decomp::THREADS, smem, b.st>>>(b.A, n, b.C, b.sq);
+  decomp::norm_kernel<<<1, decomp::THREADS, 0, b.st>>>(b.sq, uint32_t(N), b.norm, b.count);
+  if (cudaGetLastError()) return decomp_fail(DVQLS_E_CUDA, "decomposition kernel launch failed");
+  return DVQLS_OK;
+}
+}  // namespace
+
+int dvqls_pauli_coefficients(int n, const double* A, double* out_coeffs, int device) {
+  g_decomp_err.clear();
+  if (n < 1 || n > 13 || !A || !out_coeffs) return decomp_fail(DVQLS_E_ARG, "n must be in [1, 13], non-NULL buffers");
+  DecompBufs b;
+  int rc = decomp_transform(b, n, A, device);
+  if (rc) return rc;
+  const size_t NN = (size_t(1) << n) * (size_t(1) << n);
+  if (cudaMemcpyAsync(out_coeffs, b.C, sizeof(double2) * NN, cudaMemcpyDeviceToHost, b.st) ||
+      cudaStreamSynchronize(b.st))
+    return decomp_fail(DVQLS_E_CUDA, "decomposition failed");
+  return DVQLS_OK;
+}
+
+int dvqls_decompose(int n, const double* A, double eps, int64_t max_terms, char* out_paulis, double* out_coeffs,
+                    int64_t* out_L, double* out_norm, int device, float* out_ms) {
+  g_decomp_err.clear();
+  if (n < 1 || n > 13 || !A || !out_L || (max_terms > 0 && (!out_paulis || !out_coeffs)) || max_terms < 0 ||
+      !(eps >= 0.0 && eps < 1.0))
+    return decomp_fail(DVQLS_E_ARG, "n in [1, 13], 0 <= eps < 1, non-NULL outputs");
+  DecompBufs b;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int rc = decomp_transform(b, n, A, device, out_ms ? &e0 : nullptr);
+  if (rc) return rc;
+  const uint64_t N = uint64_t(1) << n, total = N * N;
+  const uint64_t cap = decomp::SORT_MAX;
+  if (cudaMalloc((void**)&b.idx, sizeof(uint64_t) * cap) || cudaMalloc((void**)&b.oc, sizeof(double2) * cap) ||
+      cudaMalloc((void**)&b.os, size_t(cap) * n))
+    return decomp_fail(DVQLS_E_CUDA, "cudaMalloc failed (pruning)");
+  decomp::prune_kernel<<<1184, 256, 0, b.st>>>(b.C, total, eps, b.norm, cap, b.count, b.idx);
+  unsigned long long L = 0;
+  double norm = 0.0;
+  if (cudaGetLastError() || cudaMemcpyAsync(&L, b.count, sizeof L, cudaMemcpyDeviceToHost, b.st) ||
+      cudaMemcpyAsync(&norm, b.norm, sizeof norm, cudaMemcpyDeviceToHost, b.st) || cudaStreamSynchronize(b.st))
+    return decomp_fail(DVQLS_E_CUDA, "pruning failed");
+  *out_L = int64_t(L);
+  if (out_norm) *out_norm = norm;
+  if (L > cap) return decomp_fail(DVQLS_E_UNSUPPORTED, "more than 4096 terms survive the pruning");
+  if (int64_t(L) > max_terms) return decomp_fail(DVQLS_E_ARG, "max_terms too small (*out_L holds the count)");
+  if (L == 0) return DVQLS_OK;
+  if (cudaFuncSetAttribute((const void*)&decomp::sort_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(decomp::SORT_SMEM)))
+    return decomp_fail(DVQLS_E_CUDA, "sort kernel smem");
+  decomp::sort_emit_kernel<<<1, decomp::THREADS, decomp::SORT_SMEM, b.st>>>(b.C, n, b.idx, b.count, b.norm, b.oc,
+                                                                             b.os);
+  if (out_ms && (cudaEventCreate(&e1) || cudaEventRecord(e1, b.st)))
+    return decomp_fail(DVQLS_E_CUDA, "event");
+  if (cudaGetLastError() ||
+      cudaMemcpyAsync(out_coeffs, b.oc, sizeof(double2) * L, cudaMemcpyDeviceToHost, b.st) ||
+      cudaMemcpyAsync(out_paulis, b.os, size_t(L) * n, cudaMemcpyDeviceToHost, b.st) || cudaStreamSynchronize(b.st))
+    return decomp_fail(DVQLS_E_CUDA, "sort/emit failed");
+  if (out_ms) {  // device time from after the H2D copy of A to the end of sort/emit
+    cudaEventElapsedTime(out_ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  return DVQLS_OK;
+}
+
+const char* dvqls_decompose_error(void) { return g_decomp_err.c_str(); }
 
 const char* dvqls_last_error(const dvqls_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_create_err.c_str();

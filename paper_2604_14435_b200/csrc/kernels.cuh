@@ -713,6 +713,30 @@ __device__ __forceinline__ void zflip_reg_rt(double2 (&v)[R], int bit) {
 template <int WARPS>
 constexpr int reg_cap() { return (65536 / (WARPS * 32)) / 8 * 8 > 255 ? 255 : (65536 / (WARPS * 32)) / 8 * 8; }
 
+// Cost-weighted static split of circuits [c0, c0 + C) over NG groups: in canonical order every
+// period of 2(n+1) circuits holds 2 denominator circuits (weight 1: gather + readout) and 2n
+// numerator circuits (weight WNUM: + two FWHTs and exchanges; ~3x the SMEM wavefronts).
+// Equal-count ranges leave whole numerator circuits of imbalance per group at small per-GPU
+// work (6 circuits per group at 8 GPUs); equal-weight ranges halve it.  Closed form, no search.
+constexpr int64_t WNUM = 3;
+__device__ __forceinline__ int64_t wcum(int64_t c, int n) {  // weight of circuits [0, c)
+  const int64_t P = 2 * int64_t(n + 1), per = 2 + 2 * int64_t(n) * WNUM;
+  const int64_t q = c / P, r = c - q * P;
+  return q * per + (r < 2 ? r : 2 + (r - 2) * WNUM);
+}
+__device__ __forceinline__ int64_t winv(int64_t w, int n) {  // smallest c with wcum(c) >= w
+  const int64_t P = 2 * int64_t(n + 1), per = 2 + 2 * int64_t(n) * WNUM;
+  const int64_t q = w / per, rem = w - q * per;
+  return q * P + (rem <= 2 ? rem : 2 + (rem - 2 + WNUM - 1) / WNUM);
+}
+__device__ __forceinline__ void weighted_range(int64_t c0, int64_t C, int64_t g, int64_t NG, int n, int64_t* b,
+                                               int64_t* e) {
+  const int64_t w0 = wcum(c0, n), tot = wcum(c0 + C, n) - w0;
+  const int64_t lo = winv(w0 + tot * g / NG, n), hi = winv(w0 + tot * (g + 1) / NG, n);
+  *b = min(max(lo - c0, int64_t(0)), C);
+  *e = g + 1 == NG ? C : min(max(hi - c0, int64_t(0)), C);
+}
+
 template <int NQ, int WARPS, bool HH>
 __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(reg_cap<WARPS>())
 hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ tab,
@@ -747,7 +771,13 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
 
   const int64_t NG = (int64_t)gridDim.x * WARPS * GPW;
   const int64_t g = ((int64_t)blockIdx.x * WARPS + warp) * GPW + gw;
-  const int cb = int(g * C / NG), ce = int((g + 1) * C / NG);  // local circuit range (C < 2^31)
+  int cb, ce;  // local circuit range (C < 2^31), cost-weighted
+  {
+    int64_t b, e;
+    weighted_range(c0, C, g, NG, NQ, &b, &e);
+    cb = int(b);
+    ce = int(e);
+  }
   const int n1 = NQ + 1;
 
   // per-group running sums (Re E, Im E, Re Psi, Im Psi) live in SMEM, not registers

@@ -34,7 +34,8 @@ EXPORTED = [
     "dvqls_local_range", "dvqls_stream", "dvqls_launches_per_call", "dvqls_last_timings",
     "dvqls_nccl_unique_id", "dvqls_build_info", "dvqls_shard_range", "dvqls_state",
     "dvqls_terms_subset", "dvqls_launch_grid", "dvqls_num_observables", "dvqls_task_observable",
-    "dvqls_costs_dev", "dvqls_global_cost",
+    "dvqls_costs_dev", "dvqls_global_cost", "dvqls_decompose", "dvqls_pauli_coefficients",
+    "dvqls_decompose_error",
 ]
 
 
@@ -93,6 +94,10 @@ def load():
     L.dvqls_launches_per_call.argtypes = [vp]
     L.dvqls_launch_grid.argtypes = [vp]
     L.dvqls_costs_dev.argtypes = [vp, ctypes.c_int, vp, vp, vp]
+    L.dvqls_decompose.argtypes = [ctypes.c_int, dp, ctypes.c_double, ctypes.c_int64, ctypes.c_char_p, dp,
+                                  ctypes.POINTER(ctypes.c_int64), dp, ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
+    L.dvqls_pauli_coefficients.argtypes = [ctypes.c_int, dp, dp, ctypes.c_int]
+    L.dvqls_decompose_error.restype = ctypes.c_char_p
     L.dvqls_global_cost.argtypes = [vp, dp, dp, dp]
     L.dvqls_num_observables.argtypes = [vp]
     L.dvqls_num_observables.restype = ctypes.c_int64
@@ -106,7 +111,7 @@ def load():
                                     ctypes.POINTER(ctypes.c_int64)]
     for name in EXPORTED:
         if name not in ("dvqls_destroy", "dvqls_last_error", "dvqls_num_circuits", "dvqls_stream",
-                        "dvqls_build_info", "dvqls_num_observables"):
+                        "dvqls_build_info", "dvqls_num_observables", "dvqls_decompose_error"):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -304,6 +309,37 @@ def dvqls_cost_batch(ctx: Context, thetas):
 
 def dvqls_destroy(ctx: Context) -> None:
     ctx.destroy()
+
+
+def decompose(A, eps: float, max_terms: int = 4096, device: int = -1, timing: bool = False):
+    """NEXT-4 on the GPU: pruned, ordered LCU [(c, pauli_string)] of a dense A, and ||c||_2
+    (and the device milliseconds with timing=True)."""
+    A = np.ascontiguousarray(A, dtype=np.complex128)
+    N = A.shape[0]
+    n = N.bit_length() - 1
+    a = A.view(np.float64).reshape(-1)
+    chars = ctypes.create_string_buffer(max_terms * n)
+    co = np.empty(2 * max_terms)
+    L, norm, ms = ctypes.c_int64(), ctypes.c_double(), ctypes.c_float()
+    rc = load().dvqls_decompose(n, _dp(a), float(eps), max_terms, chars, _dp(co), ctypes.byref(L),
+                                ctypes.byref(norm), device, ctypes.byref(ms) if timing else None)
+    if rc:
+        raise DvqlsError(rc, load().dvqls_decompose_error().decode())
+    raw = chars.raw
+    terms = [(complex(co[2 * i], co[2 * i + 1]), raw[i * n:(i + 1) * n].decode()) for i in range(L.value)]
+    return (terms, norm.value, float(ms.value)) if timing else (terms, norm.value)
+
+
+def pauli_coefficients(A, device: int = -1) -> np.ndarray:
+    """NEXT-4: all 4^n coefficients as C[m, z] (x-mask m, z-mask z)."""
+    A = np.ascontiguousarray(A, dtype=np.complex128)
+    N = A.shape[0]
+    n = N.bit_length() - 1
+    out = np.empty(2 * N * N)
+    rc = load().dvqls_pauli_coefficients(n, _dp(A.view(np.float64).reshape(-1)), _dp(out), device)
+    if rc:
+        raise DvqlsError(rc, load().dvqls_decompose_error().decode())
+    return out.view(np.complex128).reshape(N, N)
 
 
 def task_observable(n: int, pauli_l: str, pauli_k: str, s: int):

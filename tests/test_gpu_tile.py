@@ -80,9 +80,10 @@ def test_parameter_shift_pair_cost(dv):
 
 
 @pytest.mark.parametrize("n,ent", [(15, 0), (16, 1), (17, 0)])
-def test_team_mode_full(dv, n, ent):
-    """n >= 15 runs the team kernel (T CTAs per circuit, cooperative launch): full terms, cost and a
-    batch of 3 thetas against the oracle."""
+def test_team_mode_full(dv, n, ent, monkeypatch):
+    """n >= 15 with DVQLS_TEAM=1 runs the team kernel (T CTAs per circuit, cooperative launch): full
+    terms, cost and a batch of 3 thetas against the oracle."""
+    monkeypatch.setenv("DVQLS_TEAM", "1")
     w = configs.random_workload(n, 2, 2, seed=70 + n, entangler=ent)
     ctx = dv.from_workload(w, max_batch=4)
     try:
@@ -101,8 +102,11 @@ def test_team_mode_full(dv, n, ent):
         assert abs(cb[k] - ocost.cost(rk, ocost.coeffs_of(w), w.n, w.L)[0]) <= TOL
 
 
-def test_team_mode_cfg5_n16_sampled(dv):
-    """Config 5 at n = 16 through the team kernel (all 139,264 circuits), strided sample vs oracle."""
+@pytest.mark.parametrize("team", ["0", "1"])
+def test_cfg5_n16_full_sampled(dv, team, monkeypatch):
+    """Config 5 at n = 16, all 139,264 circuits (per-CTA kernel, and the team kernel with
+    DVQLS_TEAM=1), strided sample vs oracle."""
+    monkeypatch.setenv("DVQLS_TEAM", team)
     w = configs.cfg5(16)
     th = w.theta0()
     ctx = dv.from_workload(w)

@@ -63,3 +63,13 @@ def test_ordering_rule():
         if abs(mags[i] - mags[i + 1]) < 1e-13:
             assert terms[i][1] < terms[i + 1][1]  # ASCII order of I<X<Y<Z is the lexicographic rule
     assert terms[0] == (2.0 + 0j, "IIII")
+
+
+def test_single_coefficient_matches_full_transform():
+    rng = np.random.default_rng(3)
+    n = 6
+    N = 1 << n
+    A = rng.normal(size=(N, N)) + 1j * rng.normal(size=(N, N))
+    C = pauli_decomp.coefficients(A)
+    for m, z in [(0, 0), (5, 9), (63, 63), (17, 40)]:
+        assert abs(pauli_decomp.coefficient(A, m, z) - C[m, z]) < 1e-12
