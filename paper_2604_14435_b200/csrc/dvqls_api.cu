@@ -254,12 +254,12 @@ int launch_hadamard(dvqls_ctx* ctx, int K, int64_t c0, int64_t C, const int64_t*
   }
   if (ctx->tile_path && ctx->n > ctx->tile_bits) grid = std::max(1, grid / K);  // scratch: grid CTAs in total
   dim3 g(grid, K);
-  if (!ctx->tile_path) {
+  if (!ctx->tile_path) {  // one persistent 1-D grid over the flattened K x C work (kernels.cuh)
     void* args[] = {(void*)&ctx->d_x,   (void*)&ctx->d_tab, (void*)&ctx->d_coef,  (void*)&ctx->d_hv,
-                    (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&c0, (void*)&C,
+                    (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&c0, (void*)&C, (void*)&K,
                     (void*)&terms, (void*)&ctx->d_partials, (void*)&with_cost, (void*)&red_out,
                     (void*)&ctx->d_counter, (void*)&p2p};
-    CK(cudaLaunchKernel(ctx->kc.fn, g, dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
+    CK(cudaLaunchKernel(ctx->kc.fn, dim3(grid), dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
   } else {
     void* args[] = {(void*)&ctx->d_x, (void*)&ctx->d_tab, (void*)&ctx->d_coef, (void*)&ctx->d_hv,
                     (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&ctx->n, (void*)&c0, (void*)&C,

@@ -512,6 +512,47 @@ __device__ void finish_partials(const double* __restrict__ partials, int64_t NG,
   }
 }
 
+// a9/a10 for kernels whose CTAs cover (theta, circuit) ranges flattened over a batch of K
+// thetas: partials[k][G][4] holds one fixed-order quadruple per CTA and theta (zero where the CTA
+// did not touch theta).  The last CTA of the grid (ticket) sums each theta's G quadruples in CTA
+// order and writes (C, E, Psi) / (E, Psi), or runs the NVLink allreduce per theta.
+__device__ void finish_all(const double* __restrict__ partials, int G, int K, int n, int with_cost,
+                           double* __restrict__ out, unsigned* __restrict__ counter, const P2PArgs& p2p) {
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // warp w reduces thetas w, w + nwarps, ...: lanes stride the CTAs, then a fixed shuffle tree
+  for (int k = warp; k < K; k += int(blockDim.x >> 5)) {
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    for (int b = lane; b < G; b += 32) {
+      const double* p = partials + (size_t(k) * G + b) * 4;
+      a0 += __ldcg(p + 0); a1 += __ldcg(p + 1); a2 += __ldcg(p + 2); a3 += __ldcg(p + 3);
+    }
+    for (int off = 16; off >= 1; off >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, off); a1 += __shfl_xor_sync(0xffffffffu, a1, off);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, off); a3 += __shfl_xor_sync(0xffffffffu, a3, off);
+    }
+    if (lane == 0) {
+      if (p2p.world > 1) {
+        p2p_allreduce(p2p, k, n, a0, a1, a2, a3, out);
+      } else if (with_cost) {
+        double* o = out + size_t(k) * 5;
+        o[0] = cost_of_dev(a0, a2, n); o[1] = a0; o[2] = a1; o[3] = a2; o[4] = a3;
+      } else {
+        double* o = out + size_t(k) * 4;
+        o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *counter = 0u;  // ready for the next launch (stream-ordered)
+}
+
 // ---------------------------------------------------------------------------
 // a3-a9: batched Hadamard-test kernel for n = NQ system qubits.
 //
@@ -741,7 +782,7 @@ template <int NQ, int WARPS, bool HH>
 __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(reg_cap<WARPS>())
 hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ tab,
                 const double2* __restrict__ coef, const double2* __restrict__ hv, double hv_scale, int L,
-                int64_t c0, int64_t C, double* __restrict__ out_terms, double* __restrict__ partials,
+                int64_t c0, int64_t C, int K, double* __restrict__ out_terms, double* __restrict__ partials,
                 int with_cost, double* __restrict__ red_out, unsigned* __restrict__ counter, P2PArgs p2p) {
   using S = Shape<NQ>;
   constexpr int TB = S::TB, RB = S::RB, GT = S::GT, R = S::R, N = S::N, GPW = S::GPW;
@@ -751,37 +792,55 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
   double2* sbuf = smem + (HH ? 3 : 2) * N;
   double* sacc = reinterpret_cast<double*>(sbuf + (size_t)WARPS * GPW * N);  // 4 per group
 
-  const int kth = blockIdx.y;  // theta index within a batch
-  const double2* x = x_all + (size_t)kth * N;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    const double2 a = x[i];
-    sx[i] = a;
-    sx[N + i] = make_double2(-a.x, -a.y);
-  }
-  if (HH)
-    for (int i = threadIdx.x; i < N; i += blockDim.x) shv[i] = hv[i];
-  __syncthreads();
-
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = lane / GT, t = lane % GT;
   const unsigned gmask = (GT == 32) ? 0xffffffffu : (((1u << GT) - 1u) << (gw * GT));
   double2* buf = sbuf + (size_t)(warp * GPW + gw) * N;
   // byte offset of this group's exchange buffer; a multiple of 16 N when HH is false
   const uint32_t buf_off = uint32_t(reinterpret_cast<char*>(buf) - reinterpret_cast<char*>(smem));
+  constexpr int NGC = WARPS * GPW;  // circuit groups per CTA
+  const int gi = warp * GPW + gw;
+  const int n1 = NQ + 1;
+  double* acc4 = sacc + 4 * gi;  // per-group running sums (Re E, Im E, Re Psi, Im Psi)
+  if (HH)
+    for (int i = threadIdx.x; i < N; i += blockDim.x) shv[i] = hv[i];
 
-  const int64_t NG = (int64_t)gridDim.x * WARPS * GPW;
-  const int64_t g = ((int64_t)blockIdx.x * WARPS + warp) * GPW + gw;
-  int cb, ce;  // local circuit range (C < 2^31), cost-weighted
+  // ---- a3: this CTA's cost-weighted slice of the K x C (theta, circuit) work, flattened so
+  // that a batch of K thetas balances across all CTAs of one persistent grid ----
+  const int64_t G = gridDim.x;
+  const int64_t w0 = wcum(c0, NQ), Wt = wcum(c0 + C, NQ) - w0, Wall = Wt * K;
+  auto flat_of = [&](int64_t w) -> int64_t {  // first flattened circuit at weight >= w
+    if (w >= Wall) return int64_t(K) * C;
+    const int64_t th = w / Wt, rem = w - th * Wt;
+    const int64_t c = min(max(winv(w0 + rem, NQ) - c0, int64_t(0)), C);
+    return th * C + c;
+  };
+  const int64_t Fb = Wall > 0 ? flat_of(Wall * (int64_t)blockIdx.x / G) : 0;
+  const int64_t Fe = Wall <= 0 ? 0 : blockIdx.x + 1 == G ? int64_t(K) * C : flat_of(Wall * ((int64_t)blockIdx.x + 1) / G);
+  const int th_first = C > 0 ? int(Fb / C) : 0, th_last = Fe > Fb ? int((Fe - 1) / C) : th_first - 1;
+  for (int k = threadIdx.x; k < K; k += blockDim.x)  // thetas this CTA does not touch contribute 0
+    if (k < th_first || k > th_last)
+      for (int q = 0; q < 4; ++q) partials[(size_t(k) * G + blockIdx.x) * 4 + q] = 0.0;
+
+  for (int kth = th_first; kth <= th_last; ++kth) {
+  // ---- one phase per theta: stage [x, -x] of this theta, split its circuits over the groups ----
+  const int64_t pa = max(Fb, int64_t(kth) * C) - int64_t(kth) * C;
+  const int64_t pb = min(Fe, int64_t(kth + 1) * C) - int64_t(kth) * C;
+  const double2* x = x_all + (size_t)kth * N;
+  __syncthreads();  // previous phase's readers of sx are done
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const double2 a = x[i];
+    sx[i] = a;
+    sx[N + i] = make_double2(-a.x, -a.y);
+  }
+  __syncthreads();
+  int cb, ce;  // this group's circuits [cb, ce) of theta kth (local index), cost-weighted
   {
     int64_t b, e;
-    weighted_range(c0, C, g, NG, NQ, &b, &e);
-    cb = int(b);
-    ce = int(e);
+    weighted_range(c0 + pa, pb - pa, gi, NGC, NQ, &b, &e);
+    cb = int(pa + b);
+    ce = int(pa + e);
   }
-  const int n1 = NQ + 1;
-
-  // per-group running sums (Re E, Im E, Re Psi, Im Psi) live in SMEM, not registers
-  double* acc4 = sacc + 4 * (warp * GPW + gw);
   if (t == 0) acc4[0] = acc4[1] = acc4[2] = acc4[3] = 0.0;
   for (int cl = cb; cl < ce; ++cl) {
     const int64_t c = c0 + cl;
@@ -857,11 +916,15 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
       d[1] += ci;
     }
   }
-  if (t == 0) {
-    double* o = partials + ((size_t)kth * NG + g) * 4;
-    o[0] = acc4[0]; o[1] = acc4[1]; o[2] = acc4[2]; o[3] = acc4[3];
+  __syncthreads();
+  if (threadIdx.x == 0) {  // fixed group order
+    double e0 = 0, e1 = 0, e2 = 0, e3 = 0;
+    for (int q = 0; q < NGC; ++q) { e0 += sacc[4 * q]; e1 += sacc[4 * q + 1]; e2 += sacc[4 * q + 2]; e3 += sacc[4 * q + 3]; }
+    double* o = partials + ((size_t)kth * G + blockIdx.x) * 4;
+    o[0] = e0; o[1] = e1; o[2] = e2; o[3] = e3;
   }
-  if (red_out) finish_partials(partials, NG, kth, NQ, with_cost, red_out, counter, p2p.world > 1 ? &p2p : nullptr);
+  }  // theta phases
+  if (red_out) finish_all(partials, int(G), K, NQ, with_cost, red_out, counter, p2p);
 }
 
 // ---------------------------------------------------------------------------
