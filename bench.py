@@ -465,12 +465,12 @@ def main():
         for _ in range(3):
             terms, nrm, ms = dvqls.decompose(A, 0.01, device=local, timing=True)
             best = ms if best is None else min(best, ms)
-        byts = 48 * 4 ** nd
+        byts = 32 * 4 ** nd
         pk = float(load_peaks()[0]["hbm_gbs"])
         next4 = {"n": nd, "terms": len(terms), "ms": best, "GBps": byts / (best * 1e-3) / 1e9,
                  "hbm_frac": byts / (best * 1e-3) / 1e9 / pk,
-                 "note": ("NEXT-4: 4^n coefficients by per-x-mask FWHT + pruning + sort on the GPU; algorithmic "
-                          "bytes 48*4^n (A read, C written and read) over the device time (best of 3)")}
+                 "note": ("NEXT-4: 4^n coefficients by per-x-mask FWHT (norm pass + recompute-and-compact pass) + sort on the GPU; algorithmic "
+                          "bytes 32*4^n (A read twice) over the device time (best of 3)")}
         del A
 
     # ---- NEXT-2 algebraic fast path (flagged; reported separately, never the headline) ----------

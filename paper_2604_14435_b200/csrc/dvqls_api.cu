@@ -982,10 +982,13 @@ int dvqls_terms_subset(dvqls_ctx* ctx, const double* theta, const int64_t* idx, 
   return DVQLS_OK;
 }
 
+}  // extern "C"
+
 // ---- NEXT-4: Pauli decomposition + pruning (decomp.cuh) ---------------------------------------
 namespace {
 struct DecompBufs {
   double2* A = nullptr;
+  double2* B = nullptr;
   double2* C = nullptr;
   double* sq = nullptr;
   double* norm = nullptr;
@@ -995,7 +998,7 @@ struct DecompBufs {
   char* os = nullptr;
   cudaStream_t st = nullptr;
   ~DecompBufs() {
-    cudaFree(A); cudaFree(C); cudaFree(sq); cudaFree(norm); cudaFree(count); cudaFree(idx); cudaFree(oc); cudaFree(os);
+    cudaFree(A); cudaFree(B); cudaFree(C); cudaFree(sq); cudaFree(norm); cudaFree(count); cudaFree(idx); cudaFree(oc); cudaFree(os);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -1006,8 +1009,24 @@ int decomp_fail(int code, const char* msg) {
   return code;
 }
 
-// steps 1 (+ norm) of NEXT-4 on the device: C[m, z] and ||c||_2
-int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, cudaEvent_t* ev0 = nullptr) {
+// NEXT-4 device passes over B (XOR diagonals of A as rows; n < 5: straight from A)
+template <int MODE>
+void launch_rows(DecompBufs& b, int n, double eps, uint64_t cap) {
+  const unsigned N = 1u << n;
+  const int direct = n < 5 ? 1 : 0;
+  decomp::fwht_rows_kernel<MODE><<<N, decomp::THREADS, sizeof(double2) * N, b.st>>>(
+      direct ? b.A : b.B, n, b.C, b.sq, eps, b.norm, cap, b.count, b.idx, direct);
+}
+template <int MODE>
+int set_rows_smem(int n) {
+  if (cudaFuncSetAttribute((const void*)&decomp::fwht_rows_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(sizeof(double2) << n)))
+    return decomp_fail(DVQLS_E_CUDA, "fwht_rows_kernel smem");
+  return DVQLS_OK;
+}
+
+int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, bool write_c,
+                     cudaEvent_t* ev0 = nullptr) {
   if (device >= 0 && cudaSetDevice(device) != cudaSuccess) return decomp_fail(DVQLS_E_CUDA, "cudaSetDevice");
   int dev = 0;
   cudaDeviceProp prop;
@@ -1015,28 +1034,31 @@ int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, cud
     return decomp_fail(DVQLS_E_CUDA, "libdvqls is built for sm_100a only");
   const size_t N = size_t(1) << n, NN = N * N;
   if (cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking) || cudaMalloc((void**)&b.A, sizeof(double2) * NN) ||
-      cudaMalloc((void**)&b.C, sizeof(double2) * NN) || cudaMalloc((void**)&b.sq, sizeof(double) * N) ||
-      cudaMalloc((void**)&b.norm, sizeof(double)) || cudaMalloc((void**)&b.count, sizeof(unsigned long long)))
+      cudaMalloc((void**)&b.C, sizeof(double2) * (write_c ? NN : size_t(decomp::SORT_MAX))) ||
+      cudaMalloc((void**)&b.sq, sizeof(double) * N) || cudaMalloc((void**)&b.norm, sizeof(double)) ||
+      cudaMalloc((void**)&b.count, sizeof(unsigned long long)))
     return decomp_fail(DVQLS_E_CUDA, "cudaMalloc failed (decomposition)");
   if (cudaMemcpyAsync(b.A, A_host, sizeof(double2) * NN, cudaMemcpyHostToDevice, b.st))
     return decomp_fail(DVQLS_E_CUDA, "copy of A failed");
-  const size_t smem = sizeof(double2) * N;
-  if (cudaFuncSetAttribute((const void*)&decomp::fwht_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(smem)))
-    return decomp_fail(DVQLS_E_CUDA, "fwht_rows_kernel smem");
+  int rc = write_c ? set_rows_smem<0>(n) : set_rows_smem<1>(n);
+  if (rc) return rc;
+  if (n >= 5 && cudaMalloc((void**)&b.B, sizeof(double2) * NN)) return decomp_fail(DVQLS_E_CUDA, "cudaMalloc B");
   if (ev0 && (cudaEventCreate(ev0) || cudaEventRecord(*ev0, b.st))) return decomp_fail(DVQLS_E_CUDA, "event");
-  decomp::fwht_rows_kernel<<<unsigned(N), decomp::THREADS, smem, b.st>>>(b.A, n, b.C, b.sq);
+  if (n >= 5) decomp::xor_transpose_kernel<<<unsigned((N >> 5) * (N >> 5)), 256, 0, b.st>>>(b.A, n, b.B);
+  if (write_c) launch_rows<0>(b, n, 0.0, 0); else launch_rows<1>(b, n, 0.0, 0);
   decomp::norm_kernel<<<1, decomp::THREADS, 0, b.st>>>(b.sq, uint32_t(N), b.norm, b.count);
   if (cudaGetLastError()) return decomp_fail(DVQLS_E_CUDA, "decomposition kernel launch failed");
   return DVQLS_OK;
 }
 }  // namespace
 
+extern "C" {
+
 int dvqls_pauli_coefficients(int n, const double* A, double* out_coeffs, int device) {
   g_decomp_err.clear();
   if (n < 1 || n > 13 || !A || !out_coeffs) return decomp_fail(DVQLS_E_ARG, "n must be in [1, 13], non-NULL buffers");
   DecompBufs b;
-  int rc = decomp_transform(b, n, A, device);
+  int rc = decomp_transform(b, n, A, device, true);
   if (rc) return rc;
   const size_t NN = (size_t(1) << n) * (size_t(1) << n);
   if (cudaMemcpyAsync(out_coeffs, b.C, sizeof(double2) * NN, cudaMemcpyDeviceToHost, b.st) ||
@@ -1053,14 +1075,17 @@ int dvqls_decompose(int n, const double* A, double eps, int64_t max_terms, char*
     return decomp_fail(DVQLS_E_ARG, "n in [1, 13], 0 <= eps < 1, non-NULL outputs");
   DecompBufs b;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  int rc = decomp_transform(b, n, A, device, out_ms ? &e0 : nullptr);
+  int rc = decomp_transform(b, n, A, device, false, out_ms ? &e0 : nullptr);
   if (rc) return rc;
   const uint64_t N = uint64_t(1) << n, total = N * N;
   const uint64_t cap = decomp::SORT_MAX;
   if (cudaMalloc((void**)&b.idx, sizeof(uint64_t) * cap) || cudaMalloc((void**)&b.oc, sizeof(double2) * cap) ||
       cudaMalloc((void**)&b.os, size_t(cap) * n))
     return decomp_fail(DVQLS_E_CUDA, "cudaMalloc failed (pruning)");
-  decomp::prune_kernel<<<1184, 256, 0, b.st>>>(b.C, total, eps, b.norm, cap, b.count, b.idx);
+  (void)total;
+  rc = set_rows_smem<2>(n);
+  if (rc) return rc;
+  launch_rows<2>(b, n, eps, cap);
   unsigned long long L = 0;
   double norm = 0.0;
   if (cudaGetLastError() || cudaMemcpyAsync(&L, b.count, sizeof L, cudaMemcpyDeviceToHost, b.st) ||

@@ -842,13 +842,25 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
     ce = int(pa + e);
   }
   if (t == 0) acc4[0] = acc4[1] = acc4[2] = acc4[3] = 0.0;
+  // canonical decode c -> (l, k, s, part) once per phase, then advanced per circuit without
+  // divisions (64-bit division by the run-time L costs ~100 instructions per circuit)
+  int part_, s_, k_, l_;
+  {
+    const int64_t c = c0 + cb, tk = c >> 1, lk = tk / n1;
+    part_ = int(c & 1);
+    s_ = int(tk % n1);
+    k_ = int(lk % L);
+    l_ = int(lk / L);
+  }
   for (int cl = cb; cl < ce; ++cl) {
-    const int64_t c = c0 + cl;
-    const int64_t tk = c >> 1;
-    const int part = int(c & 1);
-    const int s = int(tk % n1);
-    const int64_t lk = tk / n1;
-    const int k = int(lk % L), l = int(lk / L);
+    const int part = part_, s = s_, k = k_, l = l_;
+    if (++part_ == 2) {
+      part_ = 0;
+      if (++s_ == n1) {
+        s_ = 0;
+        if (++k_ == L) { k_ = 0; ++l_; }
+      }
+    }
     const PauliTerm Tk = tab[k];
 
     // ---- a4: branch init + c-A_k: phi_i = sgn_k(i ^ m_k) x[i ^ m_k]  (layout A) ----
