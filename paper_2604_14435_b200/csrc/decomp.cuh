@@ -6,13 +6,19 @@
 // P(m, z)|k> = i^{popcount(m&z)} (-1)^{popcount(k&z)} |k ^ m> has one nonzero per column, so for a
 // fixed x-mask m the 2^n coefficients are one Walsh-Hadamard transform (over k) of the "XOR
 // diagonal" a_m[k] = A[k, k ^ m].  xor_transpose_kernel lays the diagonals out as contiguous
-// rows B[m, :] (coalesced tiles), then one CTA per m runs the FWHT in SMEM, phase and scale.
-// dvqls_decompose runs that twice (norm pass, then a bitwise-identical recompute that compacts
-// the survivors), so no 4^n coefficient array is stored: A read, B written, B read twice =
-// 64 * 4^n algorithmic bytes, all coalesced, HBM-bound.
+// rows B[m, :] (coalesced tiles) and sums |A|^2 on the way; then one CTA per m runs the FWHT
+// (n >= 9: 16 amplitudes per thread in registers, ceil(n/4) register passes joined by SMEM
+// exchanges; n <= 8: radix-2 in SMEM), phase and scale.
 //
-// Pruning keeps |c| >= 1e-14 and |c| >= eps * ||c||_2 (reading 15); survivors are compacted and
-// sorted by (round(|c| / (1e-12 ||c||_2)) descending, lexicographic I<X<Y<Z ascending) in one CTA.
+// One pass over B: Parseval, sum_P |c_P|^2 = ||A||_F^2 / 2^n, gives ||c||_2 before the FWHT up to
+// rounding, so the pass compacts every CANDIDATE |c| >= max(1e-14, eps ||A||_F / 2^{n/2} (1 - 1e-9))
+// and, in the same pass, sums |c|^2 per row in a fixed order; the exact ||c||_2 = sqrt(sum |c|^2)
+// (the definition, reading 15) then applies the pruning rule to the candidates inside the sort.
+// Traffic: A read, B written, B read = 48 * 4^n bytes, coalesced, HBM-bound; no 4^n coefficient
+// array is stored.
+//
+// Pruning keeps |c| >= 1e-14 and |c| >= eps * ||c||_2 (reading 15); survivors are sorted by
+// (round(|c| / (1e-12 ||c||_2)) descending, lexicographic I<X<Y<Z ascending) in one CTA.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -28,27 +34,112 @@ constexpr size_t SORT_SMEM = SORT_MAX * (8 + 8 + 4);
 // XOR-diagonal transposition B[m, k] = A[k, k ^ m] in 32 x 32 tiles: the tile of rows
 // [k0, k0+32) x columns [j0, j0+32) holds exactly the elements of B rows M0 + (a ^ b) (M0 =
 // (k0 ^ j0) & ~31), columns k0 + a; read along j and written along k, both coalesced.
+// fro[tile] = sum of |A|^2 over the tile (fixed order), for the Parseval candidate bound.
 __global__ void __launch_bounds__(256) xor_transpose_kernel(const double2* __restrict__ A, int n,
-                                                            double2* __restrict__ B) {
+                                                            double2* __restrict__ B, double* __restrict__ fro) {
   __shared__ double2 t[32][33];
+  __shared__ double red[8];
   const uint32_t N = 1u << n, tiles = N >> 5;
   const uint32_t k0 = (blockIdx.x / tiles) << 5, j0 = (blockIdx.x % tiles) << 5;
   const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  for (uint32_t r = ty; r < 32; r += 8) t[r][tx] = A[size_t(k0 + r) * N + j0 + tx];
+  double acc = 0.0;
+  for (uint32_t r = ty; r < 32; r += 8) {
+    const double2 a = __ldcs(A + size_t(k0 + r) * N + j0 + tx);
+    acc = fma(a.x, a.x, fma(a.y, a.y, acc));
+    t[r][tx] = a;
+  }
   __syncthreads();
   const uint32_t M0 = (k0 ^ j0) & ~31u;
   for (uint32_t ml = ty; ml < 32; ml += 8)  // row M0 + ml of B gets A[k0 + tx, j0 + (tx ^ ml)]
     B[size_t(M0 + ml) * N + k0 + tx] = t[tx][tx ^ ml];
+  for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (tx == 0) red[ty] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double f = 0.0;
+    for (int w = 0; w < 8; ++w) f += red[w];
+    fro[blockIdx.x] = f;
+  }
 }
 
-// MODE 0: write C[m, :];  MODE 1: only the CTA's sum of |c|^2 (norm pass);  MODE 2: recompute
-// and compact the survivors |c| >= max(1e-14, eps ||c||_2) (prune pass; bitwise the same values as
-// MODE 0/1, so no 4^n coefficient array is written or re-read).  Row m of B (XOR diagonal m of
-// A, contiguous) is read coalesced.  n < 5 (tiny) reads A directly.
+// n < 5 (no transposition): fro[0] = sum |A|^2, one CTA
+__global__ void __launch_bounds__(256) fro_small_kernel(const double2* __restrict__ A, uint32_t NN,
+                                                        double* __restrict__ fro) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (uint32_t i = threadIdx.x; i < NN; i += 256) acc = fma(A[i].x, A[i].x, fma(A[i].y, A[i].y, acc));
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int off = 128; off >= 1; off >>= 1) {
+    if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) fro[0] = red[0];
+}
+
+// candidate threshold from Parseval: thr0 = eps * sqrt(sum fro / 2^n) * (1 - 1e-9) (below the
+// exact eps ||c||_2 by far more than the rounding gap), floor 1e-14; zeroes the candidate counter
+__global__ void __launch_bounds__(256) prenorm_kernel(const double* __restrict__ fro, uint32_t nf, uint32_t N,
+                                                      double eps, double* __restrict__ thr0,
+                                                      unsigned long long* __restrict__ count) {
+  __shared__ double red[256];
+  double a = 0.0;
+  for (uint32_t i = threadIdx.x; i < nf; i += 256) a += fro[i];
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int off = 128; off >= 1; off >>= 1) {
+    if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *thr0 = fmax(1e-14, eps * sqrt(red[0] / double(N)) * (1.0 - 1e-9));
+    *count = 0ull;
+  }
+}
+
+// Epilogue of one coefficient c = i^{popcount(m&z)} f / 2^n (f = FWHT value):
+// MODE 0 writes C[m, z];  MODE 1 compacts candidates |c| >= *thr0 into (idx, C[slot]) and returns
+// |c|^2 for the row's fixed-order sum.
+template <int MODE>
+__device__ __forceinline__ double emit_coef(double2 f, uint32_t m, uint32_t z, uint32_t N, double inv, double thr,
+                                            double2* __restrict__ C, uint64_t cap,
+                                            unsigned long long* __restrict__ count, uint64_t* __restrict__ idx) {
+  const int q = __popc(m & z) & 3;  // i^q
+  const double re = (q == 0 ? f.x : q == 1 ? -f.y : q == 2 ? -f.x : f.y) * inv;
+  const double im = (q == 0 ? f.y : q == 1 ? f.x : q == 2 ? -f.y : -f.x) * inv;
+  if (MODE == 0) C[size_t(m) * N + z] = make_double2(re, im);
+  if (MODE == 1) {
+    const double a = sqrt(fma(re, re, im * im));
+    if (a >= thr) {
+      const unsigned long long slot = atomicAdd(count, 1ull);
+      if (slot < cap) {
+        idx[slot] = uint64_t(m) * N + z;
+        C[slot] = make_double2(re, im);
+      }
+    }
+  }
+  return fma(re, re, im * im);
+}
+
+// CTA sum of per-thread |c|^2 partials in a fixed order -> sq[blockIdx.x]
+template <int NT>
+__device__ __forceinline__ void row_sq(double acc, double* __restrict__ sq) {
+  __shared__ double red[NT / 32];
+  for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < NT / 32; ++w) t += red[w];  // fixed order
+    sq[blockIdx.x] = t;
+  }
+}
+
+// n <= 8: radix-2 FWHT of row m in SMEM (n < 5: the diagonal read straight from A)
 template <int MODE>
 __global__ void __launch_bounds__(THREADS)
 fwht_rows_kernel(const double2* __restrict__ B, int n, double2* __restrict__ C, double* __restrict__ sq,
-                 double eps, const double* __restrict__ norm, uint64_t cap, unsigned long long* __restrict__ count,
+                 const double* __restrict__ thr0, uint64_t cap, unsigned long long* __restrict__ count,
                  uint64_t* __restrict__ idx, int direct) {
   extern __shared__ double2 rows_smem[];  // dynamic: 2^n amplitudes
   __shared__ double red[THREADS / 32];
@@ -71,41 +162,76 @@ fwht_rows_kernel(const double2* __restrict__ B, int n, double2* __restrict__ C, 
     __syncthreads();
   }
   const double inv = 1.0 / double(N);
-  const double thr = MODE == 2 ? eps * *norm : 0.0;
+  const double thr = MODE == 1 ? *thr0 : 0.0;
   double acc = 0.0;
-  for (uint32_t i = threadIdx.x; i < NV * N; i += THREADS) {
-    const uint32_t m = m0 + (i >> n), z = i & (N - 1);
-    const double2 v = rows_smem[i];
-    const int q = __popc(m & z) & 3;  // i^q
-    const double re = (q == 0 ? v.x : q == 1 ? -v.y : q == 2 ? -v.x : v.y) * inv;
-    const double im = (q == 0 ? v.y : q == 1 ? v.x : q == 2 ? -v.y : -v.x) * inv;
-    if (MODE == 0) C[size_t(m) * N + z] = make_double2(re, im);
-    if (MODE == 2) {
-      const double a = sqrt(fma(re, re, im * im));
-      if (a >= 1e-14 && a >= thr) {
-        const unsigned long long slot = atomicAdd(count, 1ull);
-        if (slot < cap) {
-          idx[slot] = uint64_t(m) * N + z;
-          C[slot] = make_double2(re, im);  // survivor values, in slot order
-        }
-      }
-    }
-    acc = fma(re, re, fma(im, im, acc));
-  }
-  if (MODE == 2) return;
-  for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < THREADS / 32; ++w) t += red[w];  // fixed order
-    sq[blockIdx.x] = t;
-  }
+  for (uint32_t z = threadIdx.x; z < N; z += THREADS)
+    acc += emit_coef<MODE>(rows_smem[z], m0, z, N, inv, thr, C, cap, count, idx);
+  if (MODE == 1) row_sq<THREADS>(acc, sq);
 }
 
-// ||c||_2 = sqrt(sum_m sq[m]) in a fixed order (one CTA); also zeroes the survivor counter
-__global__ void __launch_bounds__(THREADS) norm_kernel(const double* __restrict__ sq, uint32_t N, double* norm,
-                                                       unsigned long long* count) {
+// n = NB >= 9: row m of B in registers, RG = 16 amplitudes per thread (2^(NB-4) threads).
+// Pass g puts index bits [b_g, b_g + 4) in registers (b_0 = NB - 4, b_1 = NB - 8, ..., last 0)
+// and butterflies the bits of that window not done before; consecutive passes exchange through
+// SMEM (slot(i) = i ^ ((i >> 4) & 7): conflict-free LDS.128/STS.128 in every layout).  Global
+// loads (pass 0 layout, i = r << (NB - 4) | t) are coalesced; HBM traffic = one read of the row.
+constexpr int RG = 16;
+template <int NB>
+__device__ __forceinline__ uint32_t rows_idx(uint32_t t, uint32_t r, int b) {
+  return ((t >> b) << (b + 4)) | (r << b) | (t & ((1u << b) - 1u));
+}
+__device__ __forceinline__ uint32_t rows_slot(uint32_t i) { return i ^ ((i >> 4) & 7u); }
+
+template <int NB, int MODE>
+__global__ void __launch_bounds__(1 << (NB - 4))
+fwht_rows_reg_kernel(const double2* __restrict__ B, double2* __restrict__ C, double* __restrict__ sq,
+                     const double* __restrict__ thr0, uint64_t cap, unsigned long long* __restrict__ count,
+                     uint64_t* __restrict__ idx) {
+  static_assert(NB >= 9 && NB <= 13, "register FWHT rows: 9 <= n <= 13");
+  constexpr int NT = 1 << (NB - 4);
+  constexpr uint32_t N = 1u << NB;
+  constexpr int NPASS = (NB + 3) / 4;
+  extern __shared__ double2 rows_smem[];
+  const uint32_t t = threadIdx.x, m0 = blockIdx.x;
+  double2 v[RG];
+  const double2* row = B + size_t(m0) * N;
+#pragma unroll
+  for (int r = 0; r < RG; ++r) v[r] = __ldcs(row + rows_idx<NB>(t, uint32_t(r), NB - 4));
+#pragma unroll
+  for (int g = 0; g < NPASS; ++g) {
+    const int b = NB - 4 * (g + 1) > 0 ? NB - 4 * (g + 1) : 0;  // register window [b, b + 4)
+    const int hi = NB - 4 * g;                                    // bits [lo, hi) still to do
+    if (g > 0) {
+      const int bp = NB - 4 * g > 0 ? NB - 4 * g : 0;  // previous window
+#pragma unroll
+      for (int r = 0; r < RG; ++r) rows_smem[rows_slot(rows_idx<NB>(t, uint32_t(r), bp))] = v[r];
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < RG; ++r) v[r] = rows_smem[rows_slot(rows_idx<NB>(t, uint32_t(r), b))];
+      __syncthreads();
+    }
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) {
+      if (b + bb >= hi) continue;  // done in an earlier window
+#pragma unroll
+      for (int r = 0; r < RG; ++r)
+        if (!(r & (1 << bb))) {
+          const double2 p = v[r], q = v[r | (1 << bb)];
+          v[r] = make_double2(p.x + q.x, p.y + q.y);
+          v[r | (1 << bb)] = make_double2(p.x - q.x, p.y - q.y);
+        }
+    }
+  }
+  const double inv = 1.0 / double(N);
+  const double thr = MODE == 1 ? *thr0 : 0.0;
+  double acc = 0.0;
+#pragma unroll
+  for (int r = 0; r < RG; ++r)
+    acc += emit_coef<MODE>(v[r], m0, rows_idx<NB>(t, uint32_t(r), 0), N, inv, thr, C, cap, count, idx);
+  if (MODE == 1) row_sq<NT>(acc, sq);
+}
+
+// ||c||_2 = sqrt(sum_m sq[m]) in a fixed order (one CTA)
+__global__ void __launch_bounds__(THREADS) norm_kernel(const double* __restrict__ sq, uint32_t N, double* norm) {
   __shared__ double red[THREADS];
   double a = 0.0;
   for (uint32_t i = threadIdx.x; i < N; i += THREADS) a += sq[i];
@@ -115,10 +241,7 @@ __global__ void __launch_bounds__(THREADS) norm_kernel(const double* __restrict_
     if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    *norm = sqrt(red[0]);
-    *count = 0ull;
-  }
+  if (threadIdx.x == 0) *norm = sqrt(red[0]);
 }
 
 // lexicographic code of P(m, z): 2 bits per qubit from qubit 0 (MSB), I=0 X=1 Y=2 Z=3
@@ -132,34 +255,43 @@ __device__ __forceinline__ uint64_t lex_code(uint32_t m, uint32_t z, int n) {
   return code;
 }
 
-// one CTA: bitonic sort of the L survivors (values C[slot], indices idx[slot] from MODE 2) by (quantised |c| desc, lex asc), then write the
-// coefficients and the Pauli strings (n chars each) in that order
+// one CTA: keep the candidates (values C[slot], indices idx[slot] from MODE 1) with |c| >= max(1e-14,
+// eps ||c||_2), bitonic-sort them by (quantised |c| desc, lex asc), write the coefficients and the
+// Pauli strings (n chars each) in that order and the survivor count *out_L
 __global__ void __launch_bounds__(THREADS)
 sort_emit_kernel(const double2* __restrict__ C, int n, const uint64_t* __restrict__ idx,
-                 const unsigned long long* __restrict__ count, const double* __restrict__ norm,
-                 double2* __restrict__ out_c, char* __restrict__ out_s) {
+                 const unsigned long long* __restrict__ count, const double* __restrict__ norm, double eps,
+                 double2* __restrict__ out_c, char* __restrict__ out_s, unsigned long long* __restrict__ out_L) {
   extern __shared__ uint64_t sort_smem[];  // dynamic: SORT_MAX * 20 B
   uint64_t* kq = sort_smem;
   uint64_t* kl = sort_smem + SORT_MAX;
   uint32_t* ki = reinterpret_cast<uint32_t*>(sort_smem + 2 * SORT_MAX);
-  const uint32_t L = uint32_t(*count);
+  const uint32_t L = uint32_t(min(*count, (unsigned long long)SORT_MAX));  // candidates
   uint32_t P = 1;
   while (P < L) P <<= 1;
   const uint32_t N = 1u << n;
   const double q = 1e-12 * *norm;
+  const double thr = fmax(1e-14, eps * *norm);  // the pruning rule with the exact ||c||_2
+  int kept = 0;
   for (uint32_t i = threadIdx.x; i < P; i += THREADS) {
-    if (i < L) {
+    const double2 c = i < L ? C[i] : make_double2(0.0, 0.0);
+    const double a = sqrt(fma(c.x, c.x, c.y * c.y));
+    if (i < L && a >= thr) {
       const uint64_t id = idx[i];
-      const double2 c = C[i];
-      const double a = sqrt(fma(c.x, c.x, c.y * c.y));
       kq[i] = ~uint64_t(llround(a / q));  // descending magnitude
       kl[i] = lex_code(uint32_t(id / N), uint32_t(id % N), n);
       ki[i] = i;
+      ++kept;
     } else {
-      kq[i] = ~0ull; kl[i] = ~0ull; ki[i] = 0xffffffffu;  // padding sorts last
+      kq[i] = ~0ull; kl[i] = ~0ull; ki[i] = 0xffffffffu;  // dropped candidates and padding sort last
     }
   }
+  __shared__ unsigned s_kept;
+  if (threadIdx.x == 0) s_kept = 0u;
   __syncthreads();
+  if (kept) atomicAdd(&s_kept, unsigned(kept));
+  __syncthreads();
+  const uint32_t LK = s_kept;
   for (uint32_t k = 2; k <= P; k <<= 1) {
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
       for (uint32_t i = threadIdx.x; i < P; i += THREADS) {
@@ -177,7 +309,8 @@ sort_emit_kernel(const double2* __restrict__ C, int n, const uint64_t* __restric
       __syncthreads();
     }
   }
-  for (uint32_t r = threadIdx.x; r < L; r += THREADS) {
+  if (threadIdx.x == 0) *out_L = LK;
+  for (uint32_t r = threadIdx.x; r < LK; r += THREADS) {
     const uint64_t id = idx[ki[r]];
     out_c[r] = C[ki[r]];
     const uint32_t m = uint32_t(id / N), z = uint32_t(id % N);

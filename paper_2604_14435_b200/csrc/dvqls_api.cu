@@ -22,6 +22,7 @@
 
 #include "../../include/dvqls.h"
 #include "kernels.cuh"
+#include "plane.cuh"
 #include "tile.cuh"
 #include "stream.cuh"
 #include "pauli.cuh"
@@ -42,6 +43,7 @@ struct KernelCfg {
   int warps = 0;
   size_t smem = 0;
   int gpw = 0;  // circuit groups per warp
+  int groups = 0;  // circuit groups per CTA
 };
 
 template <int NQ, bool HH, int W>
@@ -53,6 +55,28 @@ KernelCfg make_cfg() {
   k.gpw = S::GPW;
   k.smem = sizeof(double2) * (size_t(HH ? 3 : 2) * S::N + size_t(W) * S::GPW * S::N) +
            sizeof(double) * 4 * size_t(W) * S::GPW;
+  k.groups = W * S::GPW;
+  return k;
+}
+
+// n = 10, uniform b: the real-plane kernel (plane.cuh), one circuit per warp pair
+template <int W>
+KernelCfg make_plane_cfg() {
+  KernelCfg k;
+  k.fn = (const void*)&plane::plane_kernel<W>;
+  k.warps = W;
+  k.gpw = 1;
+  k.groups = W / 2;
+  // the x planes sit at a 16 KB-aligned shared-window address inside the allocation: size it
+  // for the actual dynamic base (reserved SMEM + this kernel's static SMEM); the kernel traps
+  // if the base differs
+  cudaFuncAttributes fa{};
+  int dev = 0, reserved = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+  cudaFuncGetAttributes(&fa, k.fn);
+  const uint32_t sb = uint32_t(reserved) + ((uint32_t(fa.sharedSizeBytes) + 15u) & ~15u);
+  k.smem = plane::smem_bytes<W>(sb);
   return k;
 }
 
@@ -64,6 +88,18 @@ KernelCfg make_cfg() {
 // DVQLS_WARPS=8 forces the 8-warp variant (tuning knob).
 template <int NQ, bool HH>
 KernelCfg pick_cfg() {
+  if constexpr (NQ == 10 && !HH) {
+    // DVQLS_PLANE=0 selects the complex-layout kernel (A/B comparison knob)
+    const char* pe = getenv("DVQLS_PLANE");
+    if (!pe || atoi(pe) != 0) {
+      const char* e = getenv("DVQLS_WARPS");
+      const int w = e ? atoi(e) : 20;
+      // registers are split per SM sub-partition (16K each): 16 warps (4 per scheduler, <= 128
+      // registers) or 20 (5 per scheduler, <= 96); measured on B200, 20 is faster
+      if (w == 16) return make_plane_cfg<16>();
+      return make_plane_cfg<20>();
+    }
+  }
   if constexpr (NQ >= 9) {
     const char* e = getenv("DVQLS_WARPS");
     const int w = e ? atoi(e) : 12;
@@ -573,6 +609,7 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
                       : (const void*)&stream::stream_hadamard_kernel<12, false>;
     ctx->kc.warps = (1 << ctx->tile_bits) / 16 / 32;
     ctx->kc.gpw = 1;
+    ctx->kc.groups = 1;
     ctx->kc.smem = sizeof(double2) * (size_t(1) << ctx->tile_bits);
   }
   if (cudaFuncSetAttribute(ctx->kc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->kc.smem)) !=
@@ -591,7 +628,7 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   dvqls_shard_range(ctx->C, ctx->rank, ctx->world, &ctx->c0, &ctx->c1);
   ctx->chunk = (ctx->C + ctx->world - 1) / ctx->world;
   const int64_t Cloc = ctx->c1 - ctx->c0;
-  const int64_t groups_per_cta = ctx->tile_path ? 1 : int64_t(ctx->kc.warps) * ctx->kc.gpw;
+  const int64_t groups_per_cta = ctx->tile_path ? 1 : int64_t(ctx->kc.groups);
   int64_t want = int64_t(prop.multiProcessorCount) * occ;
   if (ctx->tile_path && n > ctx->tile_bits) {  // each CTA owns a 2^n-amplitude global scratch
     const int64_t cap = int64_t(kScratchBudget / (sizeof(double2) * size_t(ctx->N)));
@@ -992,13 +1029,17 @@ struct DecompBufs {
   double2* C = nullptr;
   double* sq = nullptr;
   double* norm = nullptr;
+  double* thr0 = nullptr;
+  double* fro = nullptr;
   unsigned long long* count = nullptr;
+  unsigned long long* outL = nullptr;
   uint64_t* idx = nullptr;
   double2* oc = nullptr;
   char* os = nullptr;
   cudaStream_t st = nullptr;
   ~DecompBufs() {
     cudaFree(A); cudaFree(B); cudaFree(C); cudaFree(sq); cudaFree(norm); cudaFree(count); cudaFree(idx); cudaFree(oc); cudaFree(os);
+    cudaFree(thr0); cudaFree(fro); cudaFree(outL);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -1009,23 +1050,41 @@ int decomp_fail(int code, const char* msg) {
   return code;
 }
 
-// NEXT-4 device passes over B (XOR diagonals of A as rows; n < 5: straight from A)
-template <int MODE>
-void launch_rows(DecompBufs& b, int n, double eps, uint64_t cap) {
-  const unsigned N = 1u << n;
-  const int direct = n < 5 ? 1 : 0;
-  decomp::fwht_rows_kernel<MODE><<<N, decomp::THREADS, sizeof(double2) * N, b.st>>>(
-      direct ? b.A : b.B, n, b.C, b.sq, eps, b.norm, cap, b.count, b.idx, direct);
+// NEXT-4 device pass over B (XOR diagonals of A as rows; n < 5: straight from A).
+// MODE 0: all coefficients into C;  MODE 1: candidates + per-row |c|^2 (decomp.cuh).
+template <int NB, int MODE>
+int launch_rows_reg(DecompBufs& b, uint64_t cap) {
+  const void* fn = (const void*)&decomp::fwht_rows_reg_kernel<NB, MODE>;
+  const int smem = int(sizeof(double2) << NB);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
+    return decomp_fail(DVQLS_E_CUDA, "fwht_rows_reg_kernel smem");
+  decomp::fwht_rows_reg_kernel<NB, MODE><<<1u << NB, 1u << (NB - 4), smem, b.st>>>(b.B, b.C, b.sq, b.thr0, cap,
+                                                                                  b.count, b.idx);
+  return DVQLS_OK;
 }
 template <int MODE>
-int set_rows_smem(int n) {
+int launch_rows(DecompBufs& b, int n, uint64_t cap) {
+  switch (n) {
+    case 9: return launch_rows_reg<9, MODE>(b, cap);
+    case 10: return launch_rows_reg<10, MODE>(b, cap);
+    case 11: return launch_rows_reg<11, MODE>(b, cap);
+    case 12: return launch_rows_reg<12, MODE>(b, cap);
+    case 13: return launch_rows_reg<13, MODE>(b, cap);
+    default: break;
+  }
+  const unsigned N = 1u << n;
+  const int direct = n < 5 ? 1 : 0;
   if (cudaFuncSetAttribute((const void*)&decomp::fwht_rows_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(sizeof(double2) << n)))
     return decomp_fail(DVQLS_E_CUDA, "fwht_rows_kernel smem");
+  decomp::fwht_rows_kernel<MODE><<<N, decomp::THREADS, sizeof(double2) * N, b.st>>>(
+      direct ? b.A : b.B, n, b.C, b.sq, b.thr0, cap, b.count, b.idx, direct);
   return DVQLS_OK;
 }
 
-int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, bool write_c,
+// A -> device, XOR-diagonal transposition (+ |A|^2 tile sums); write_c: every coefficient into C,
+// else: Parseval candidate bound, one candidate pass, exact norm (decomp.cuh)
+int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, bool write_c, double eps = 0.0,
                      cudaEvent_t* ev0 = nullptr) {
   if (device >= 0 && cudaSetDevice(device) != cudaSuccess) return decomp_fail(DVQLS_E_CUDA, "cudaSetDevice");
   int dev = 0;
@@ -1033,20 +1092,35 @@ int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, boo
   if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10)
     return decomp_fail(DVQLS_E_CUDA, "libdvqls is built for sm_100a only");
   const size_t N = size_t(1) << n, NN = N * N;
+  const size_t nfro = n >= 5 ? (N >> 5) * (N >> 5) : 1;
+  const uint64_t cap = decomp::SORT_MAX;
   if (cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking) || cudaMalloc((void**)&b.A, sizeof(double2) * NN) ||
-      cudaMalloc((void**)&b.C, sizeof(double2) * (write_c ? NN : size_t(decomp::SORT_MAX))) ||
+      cudaMalloc((void**)&b.C, sizeof(double2) * (write_c ? NN : size_t(cap))) ||
       cudaMalloc((void**)&b.sq, sizeof(double) * N) || cudaMalloc((void**)&b.norm, sizeof(double)) ||
-      cudaMalloc((void**)&b.count, sizeof(unsigned long long)))
+      cudaMalloc((void**)&b.thr0, sizeof(double)) || cudaMalloc((void**)&b.fro, sizeof(double) * nfro) ||
+      cudaMalloc((void**)&b.count, sizeof(unsigned long long)) ||
+      cudaMalloc((void**)&b.outL, sizeof(unsigned long long)))
     return decomp_fail(DVQLS_E_CUDA, "cudaMalloc failed (decomposition)");
+  if (!write_c && (cudaMalloc((void**)&b.idx, sizeof(uint64_t) * cap) ||
+                   cudaMalloc((void**)&b.oc, sizeof(double2) * cap) || cudaMalloc((void**)&b.os, size_t(cap) * n)))
+    return decomp_fail(DVQLS_E_CUDA, "cudaMalloc failed (pruning)");
   if (cudaMemcpyAsync(b.A, A_host, sizeof(double2) * NN, cudaMemcpyHostToDevice, b.st))
     return decomp_fail(DVQLS_E_CUDA, "copy of A failed");
-  int rc = write_c ? set_rows_smem<0>(n) : set_rows_smem<1>(n);
-  if (rc) return rc;
   if (n >= 5 && cudaMalloc((void**)&b.B, sizeof(double2) * NN)) return decomp_fail(DVQLS_E_CUDA, "cudaMalloc B");
   if (ev0 && (cudaEventCreate(ev0) || cudaEventRecord(*ev0, b.st))) return decomp_fail(DVQLS_E_CUDA, "event");
-  if (n >= 5) decomp::xor_transpose_kernel<<<unsigned((N >> 5) * (N >> 5)), 256, 0, b.st>>>(b.A, n, b.B);
-  if (write_c) launch_rows<0>(b, n, 0.0, 0); else launch_rows<1>(b, n, 0.0, 0);
-  decomp::norm_kernel<<<1, decomp::THREADS, 0, b.st>>>(b.sq, uint32_t(N), b.norm, b.count);
+  if (n >= 5)
+    decomp::xor_transpose_kernel<<<unsigned(nfro), 256, 0, b.st>>>(b.A, n, b.B, b.fro);
+  else
+    decomp::fro_small_kernel<<<1, 256, 0, b.st>>>(b.A, uint32_t(NN), b.fro);
+  int rc;
+  if (write_c) {
+    rc = launch_rows<0>(b, n, 0);
+  } else {
+    decomp::prenorm_kernel<<<1, 256, 0, b.st>>>(b.fro, uint32_t(nfro), uint32_t(N), eps, b.thr0, b.count);
+    rc = launch_rows<1>(b, n, cap);
+    if (!rc) decomp::norm_kernel<<<1, decomp::THREADS, 0, b.st>>>(b.sq, uint32_t(N), b.norm);
+  }
+  if (rc) return rc;
   if (cudaGetLastError()) return decomp_fail(DVQLS_E_CUDA, "decomposition kernel launch failed");
   return DVQLS_OK;
 }
@@ -1075,37 +1149,31 @@ int dvqls_decompose(int n, const double* A, double eps, int64_t max_terms, char*
     return decomp_fail(DVQLS_E_ARG, "n in [1, 13], 0 <= eps < 1, non-NULL outputs");
   DecompBufs b;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  int rc = decomp_transform(b, n, A, device, false, out_ms ? &e0 : nullptr);
+  int rc = decomp_transform(b, n, A, device, false, eps, out_ms ? &e0 : nullptr);
   if (rc) return rc;
-  const uint64_t N = uint64_t(1) << n, total = N * N;
-  const uint64_t cap = decomp::SORT_MAX;
-  if (cudaMalloc((void**)&b.idx, sizeof(uint64_t) * cap) || cudaMalloc((void**)&b.oc, sizeof(double2) * cap) ||
-      cudaMalloc((void**)&b.os, size_t(cap) * n))
-    return decomp_fail(DVQLS_E_CUDA, "cudaMalloc failed (pruning)");
-  (void)total;
-  rc = set_rows_smem<2>(n);
-  if (rc) return rc;
-  launch_rows<2>(b, n, eps, cap);
-  unsigned long long L = 0;
-  double norm = 0.0;
-  if (cudaGetLastError() || cudaMemcpyAsync(&L, b.count, sizeof L, cudaMemcpyDeviceToHost, b.st) ||
-      cudaMemcpyAsync(&norm, b.norm, sizeof norm, cudaMemcpyDeviceToHost, b.st) || cudaStreamSynchronize(b.st))
-    return decomp_fail(DVQLS_E_CUDA, "pruning failed");
-  *out_L = int64_t(L);
-  if (out_norm) *out_norm = norm;
-  if (L > cap) return decomp_fail(DVQLS_E_UNSUPPORTED, "more than 4096 terms survive the pruning");
-  if (int64_t(L) > max_terms) return decomp_fail(DVQLS_E_ARG, "max_terms too small (*out_L holds the count)");
-  if (L == 0) return DVQLS_OK;
   if (cudaFuncSetAttribute((const void*)&decomp::sort_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(decomp::SORT_SMEM)))
     return decomp_fail(DVQLS_E_CUDA, "sort kernel smem");
-  decomp::sort_emit_kernel<<<1, decomp::THREADS, decomp::SORT_SMEM, b.st>>>(b.C, n, b.idx, b.count, b.norm, b.oc,
-                                                                             b.os);
+  decomp::sort_emit_kernel<<<1, decomp::THREADS, decomp::SORT_SMEM, b.st>>>(b.C, n, b.idx, b.count, b.norm, eps,
+                                                                             b.oc, b.os, b.outL);
   if (out_ms && (cudaEventCreate(&e1) || cudaEventRecord(e1, b.st)))
     return decomp_fail(DVQLS_E_CUDA, "event");
-  if (cudaGetLastError() ||
-      cudaMemcpyAsync(out_coeffs, b.oc, sizeof(double2) * L, cudaMemcpyDeviceToHost, b.st) ||
-      cudaMemcpyAsync(out_paulis, b.os, size_t(L) * n, cudaMemcpyDeviceToHost, b.st) || cudaStreamSynchronize(b.st))
+  unsigned long long cand = 0, L = 0;
+  double norm = 0.0;
+  if (cudaGetLastError() || cudaMemcpyAsync(&cand, b.count, sizeof cand, cudaMemcpyDeviceToHost, b.st) ||
+      cudaMemcpyAsync(&L, b.outL, sizeof L, cudaMemcpyDeviceToHost, b.st) ||
+      cudaMemcpyAsync(&norm, b.norm, sizeof norm, cudaMemcpyDeviceToHost, b.st) || cudaStreamSynchronize(b.st))
+    return decomp_fail(DVQLS_E_CUDA, "pruning failed");
+  if (out_norm) *out_norm = norm;
+  if (cand > decomp::SORT_MAX) {
+    *out_L = int64_t(cand);
+    return decomp_fail(DVQLS_E_UNSUPPORTED, "more than 4096 terms survive the pruning");
+  }
+  *out_L = int64_t(L);
+  if (int64_t(L) > max_terms) return decomp_fail(DVQLS_E_ARG, "max_terms too small (*out_L holds the count)");
+  if (L > 0 && (cudaMemcpyAsync(out_coeffs, b.oc, sizeof(double2) * L, cudaMemcpyDeviceToHost, b.st) ||
+                cudaMemcpyAsync(out_paulis, b.os, size_t(L) * n, cudaMemcpyDeviceToHost, b.st) ||
+                cudaStreamSynchronize(b.st)))
     return decomp_fail(DVQLS_E_CUDA, "sort/emit failed");
   if (out_ms) {  // device time from after the H2D copy of A to the end of sort/emit
     cudaEventElapsedTime(out_ms, e0, e1);

@@ -22,7 +22,7 @@ def dv():
     return dvqls
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 9, 10])
 def test_all_coefficients_random(dv, n):
     rng = np.random.default_rng(100 + n)
     N = 1 << n
@@ -31,7 +31,8 @@ def test_all_coefficients_random(dv, n):
     assert np.max(np.abs(got - opd.coefficients(A))) <= 1e-12 * max(1.0, np.abs(A).max())
 
 
-@pytest.mark.parametrize("n,eps", [(4, 0.01), (6, 0.01), (8, 0.01), (10, 0.01), (10, 0.005)])
+@pytest.mark.parametrize("n,eps", [(4, 0.01), (6, 0.01), (8, 0.01), (9, 0.01), (10, 0.01), (10, 0.005),
+                                   (11, 0.01), (12, 0.01)])
 def test_pruned_tridiagonal(dv, n, eps):
     A, _ = problems.tridiag_toeplitz(n, 2.0, -1.0, -1.0)
     got, norm = dv.decompose(A, eps)
@@ -50,13 +51,15 @@ def test_pruned_hele_shaw(dv, which):
     assert max(abs(a - b) for (a, _), (b, _) in zip(got, ref)) <= 1e-12
 
 
-def test_pruned_random_dense(dv):
+@pytest.mark.parametrize("n,eps", [(7, 0.015), (9, 0.0055)])
+def test_pruned_random_dense(dv, n, eps):
+    """Dense random A: many coefficients near the threshold, so the Parseval candidate bound and
+    the exact-norm filter of the one-pass pruning are both exercised."""
     rng = np.random.default_rng(5)
-    n = 7
     N = 1 << n
     A = rng.normal(size=(N, N)) + 1j * rng.normal(size=(N, N))
-    got, _ = dv.decompose(A, 0.015)
-    ref, _ = opd.decompose_pruned(A, 0.015)
+    got, _ = dv.decompose(A, eps)
+    ref, _ = opd.decompose_pruned(A, eps)
     assert len(got) == len(ref) > 0
     assert [s for _, s in got] == [s for _, s in ref]
     assert max(abs(a - b) for (a, _), (b, _) in zip(got, ref)) <= 1e-12
