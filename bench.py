@@ -556,7 +556,8 @@ def main():
             "roofline": streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, ctx.grid()) if w.n > 12 else
             onchip_roofline(w, local_c, KT, had_ms, sms, fmax, peak_src) if w.n > 10 else {
                 "bound": "alu",
-                "kernel": "hadamard_kernel",
+                "kernel": ("plane_kernel<20>" if w.n == 10 and w.bkind == 0 and os.environ.get("DVQLS_PLANE", "1") != "0"
+                           else "hadamard_kernel"),
                 "achieved": achieved_ops / 1e12,
                 "peak": fp64_peak / 1e12,
                 "unit": "Top/s",
