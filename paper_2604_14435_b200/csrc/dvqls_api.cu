@@ -25,6 +25,7 @@
 #include "plane.cuh"
 #include "tile.cuh"
 #include "stream.cuh"
+#include "stream_plane.cuh"
 #include "pauli.cuh"
 #include "global.cuh"
 #include "decomp.cuh"
@@ -170,7 +171,9 @@ struct dvqls_ctx {
   double* d_team_acc = nullptr;  // nteams * 2 * team
   unsigned* d_team_ctr = nullptr;  // nteams barrier counters + 1 error flag
   int tile_bits = 12;            // tile path: amplitudes per SMEM tile = 2^tile_bits
-  double2* d_scratch = nullptr;  // grid * N (n > 12)
+  double2* d_scratch = nullptr;  // grid * N (n > 12; doubles when pstream)
+  bool pstream = false;          // n >= 11, uniform b: real-plane streaming kernel (stream_plane.cuh)
+  double* d_xp = nullptr;        // planar copy of x for pstream: [K][re N | im N]
   double2* d_x2 = nullptr;       // ring ping-pong buffer (n > 12 prefix)
   double2* d_gates = nullptr;    // fused-gate table (n > 12 prefix)
   int64_t* d_cidx = nullptr;     // circuit subset (dvqls_terms_subset)
@@ -296,6 +299,14 @@ int launch_hadamard(dvqls_ctx* ctx, int K, int64_t c0, int64_t C, const int64_t*
                     (void*)&terms, (void*)&ctx->d_partials, (void*)&with_cost, (void*)&red_out,
                     (void*)&ctx->d_counter, (void*)&p2p};
     CK(cudaLaunchKernel(ctx->kc.fn, dim3(grid), dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
+  } else if (ctx->pstream) {  // planar x, then the real-plane streaming kernel
+    streamp::to_planar_kernel<<<std::min<int64_t>(1184, (int64_t(K) * ctx->N + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->d_x, uint32_t(ctx->N), uint32_t(K), ctx->d_xp);
+    double* scr = reinterpret_cast<double*>(ctx->d_scratch);
+    void* args[] = {(void*)&ctx->d_xp, (void*)&ctx->d_tab, (void*)&ctx->d_coef, (void*)&ctx->L, (void*)&ctx->n,
+                    (void*)&c0, (void*)&C, (void*)&cidx, (void*)&scr, (void*)&terms, (void*)&ctx->d_partials,
+                    (void*)&with_cost, (void*)&red_out, (void*)&ctx->d_counter, (void*)&p2p};
+    CK(cudaLaunchKernel(ctx->kc.fn, g, dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
   } else {
     void* args[] = {(void*)&ctx->d_x, (void*)&ctx->d_tab, (void*)&ctx->d_coef, (void*)&ctx->d_hv,
                     (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&ctx->n, (void*)&c0, (void*)&C,
@@ -391,7 +402,7 @@ void release(dvqls_ctx* c) {
   cudaFree(c->d_obs); cudaFree(c->d_wE); cudaFree(c->d_wP); cudaFree(c->d_task); cudaFree(c->d_e);
   cudaFree(c->d_team_acc); cudaFree(c->d_team_ctr);
   cudaFree(c->d_b); cudaFree(c->d_beta); cudaFree(c->d_out6); cudaFree(c->d_gcounter);
-  cudaFree(c->d_counter); cudaFree(c->d_scratch); cudaFree(c->d_x2); cudaFree(c->d_gates); cudaFree(c->d_cidx); cudaFree(c->d_sub);
+  cudaFree(c->d_counter); cudaFree(c->d_scratch); cudaFree(c->d_xp); cudaFree(c->d_x2); cudaFree(c->d_gates); cudaFree(c->d_cidx); cudaFree(c->d_sub);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -611,6 +622,15 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
     ctx->kc.gpw = 1;
     ctx->kc.groups = 1;
     ctx->kc.smem = sizeof(double2) * (size_t(1) << ctx->tile_bits);
+    // uniform b: the real-plane kernel (half the registers per thread, 3 CTAs/SM instead of 2);
+    // DVQLS_PLANE=0 selects the complex kernel (A/B comparison knob)
+    const char* pe = getenv("DVQLS_PLANE");
+    if (!hh && !(pe && atoi(pe) == 0) && ctx->mode == DVQLS_MODE_CIRCUITS) {
+      ctx->pstream = true;
+      ctx->kc.fn = ctx->tile_bits == 11 ? (const void*)&streamp::stream_plane_kernel<11>
+                                        : (const void*)&streamp::stream_plane_kernel<12>;
+      ctx->kc.smem = ctx->tile_bits == 11 ? streamp::tile_smem<11>() : streamp::tile_smem<12>();
+    }
   }
   if (cudaFuncSetAttribute(ctx->kc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->kc.smem)) !=
       cudaSuccess) {
@@ -631,7 +651,7 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   const int64_t groups_per_cta = ctx->tile_path ? 1 : int64_t(ctx->kc.groups);
   int64_t want = int64_t(prop.multiProcessorCount) * occ;
   if (ctx->tile_path && n > ctx->tile_bits) {  // each CTA owns a 2^n-amplitude global scratch
-    const int64_t cap = int64_t(kScratchBudget / (sizeof(double2) * size_t(ctx->N)));
+    const int64_t cap = int64_t(kScratchBudget / ((ctx->pstream ? sizeof(double) : sizeof(double2)) * size_t(ctx->N)));
     want = std::max<int64_t>(1, std::min(want, cap));
   }
   if (ctx->tile_path) {
@@ -663,6 +683,7 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
     while (T < ratio && T * 2 <= G) T *= 2;
     T = std::min<int64_t>(T, int64_t(ctx->N >> 12));  // at most one tile per member and pass
     if (T >= 2) {
+      ctx->pstream = false;  // team mode runs the complex kernel
       ctx->team = int(T);
       ctx->nteams = int(G / T);
       ctx->grid = ctx->nteams * ctx->team;
@@ -743,7 +764,7 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
                                     (const void*)&prefix_quad_kernel<9>, (const void*)&prefix_quad_kernel<10>};
     ctx->prefix_fn = quads[n];
     ctx->prefix_threads = std::max(32, ctx->N / 4);
-    ctx->prefix_smem = sizeof(double2) * (size_t(ctx->N) + 2 * size_t(n) * layers) + sizeof(int) * ctx->N;
+    ctx->prefix_smem = sizeof(double2) * (2 * size_t(ctx->N) + 2 * size_t(n) * layers) + sizeof(int) * ctx->N;
   } else if (ctx->prefix_rb == 0) {  // one amplitude per thread, shuffles + 2 transposes per layer
     static const void* lanes[11] = {nullptr,
                                     (const void*)&prefix_lanes_kernel<1>, (const void*)&prefix_lanes_kernel<2>,
@@ -766,6 +787,17 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
     fail(ctx, DVQLS_E_CUDA, "prefix kernel smem %zu B", ctx->prefix_smem);
     return bail(DVQLS_E_CUDA);
   }
+  // The prefix and the Hadamard-test kernel run back to back every call: give both the maximum
+  // SMEM carveout so the SMs do not repartition L1/SMEM between them (DVQLS_CARVEOUT=0: driver
+  // default, A/B knob)
+  if (!(getenv("DVQLS_CARVEOUT") && atoi(getenv("DVQLS_CARVEOUT")) == 0)) {
+    if (ctx->prefix_fn)
+      cudaFuncSetAttribute(ctx->prefix_fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           int(cudaSharedmemCarveoutMaxShared));
+    cudaFuncSetAttribute(ctx->kc.fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         int(cudaSharedmemCarveoutMaxShared));
+    cudaGetLastError();
+  }
 
   // ---- device buffers (the library's only allocations) -----------------------
   const int KB = ctx->max_batch;
@@ -784,7 +816,9 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
       alloc((void**)&ctx->d_out6, sizeof(double) * 6 * KB) ||
       (ctx->bkind == DVQLS_B_AMPLITUDES && alloc((void**)&ctx->d_b, sizeof(double2) * ctx->N)) ||
       (n > 12 && ctx->mode == DVQLS_MODE_CIRCUITS &&
-       alloc((void**)&ctx->d_scratch, sizeof(double2) * size_t(ctx->team ? ctx->nteams : ctx->grid) * ctx->N)) ||
+       alloc((void**)&ctx->d_scratch, (ctx->pstream ? sizeof(double) : sizeof(double2)) *
+                                           size_t(ctx->team ? ctx->nteams : ctx->grid) * ctx->N)) ||
+      (ctx->pstream && alloc((void**)&ctx->d_xp, sizeof(double2) * KB * ctx->N)) ||
       (ctx->team && (alloc((void**)&ctx->d_team_acc, sizeof(double) * 2 * size_t(ctx->nteams) * ctx->team) ||
                      alloc((void**)&ctx->d_team_ctr, sizeof(unsigned) * (size_t(ctx->nteams) + 1)))) ||
       (ctx->mode == DVQLS_MODE_PAULI &&
@@ -1238,7 +1272,7 @@ int dvqls_launches_per_call(const dvqls_ctx* ctx) {
   // prefix (1, or 2 + layers*(groups+1) for the global n > 12 prefix), hadamard (+ fused
   // reduction) [, finalize]  (+ NCCL's own allreduce kernel when world > 1)
   const int pre = ctx->prefix_rb < 0 ? 2 + ctx->layers * ((ctx->n <= 21 ? 2 : 3) + 1) : 1;
-  return pre + 1 + ((ctx->world == 1 || ctx->p2p) ? 0 : 1);
+  return pre + 1 + (ctx->pstream ? 1 : 0) + ((ctx->world == 1 || ctx->p2p) ? 0 : 1);
 }
 
 int dvqls_last_timings(const dvqls_ctx* c, float* ms) {

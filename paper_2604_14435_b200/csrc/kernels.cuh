@@ -297,8 +297,9 @@ prefix_quad_kernel(int layers, int entangler, const double* __restrict__ thetas,
   extern __shared__ double2 qsm[];
   const int P = 3 * n * layers;
   const int G = n * layers;
-  double2* sbuf = qsm;                            // N amplitudes (transposes)
-  double2* tabU = qsm + N;                        // 2 per gate: a, b of U = [[a, -b*], [b, a*]]
+  double2* sbuf0 = qsm;                           // 2 x N amplitudes: the two transposes of a
+  double2* sbuf1 = qsm + N;                       // layer use different buffers (1 barrier each)
+  double2* tabU = qsm + 2 * N;                    // 2 per gate: a, b of U = [[a, -b*], [b, a*]]
   int* perm = reinterpret_cast<int*>(tabU + 2 * G);
   const double* th = thetas + (size_t)blockIdx.x * P;
   const int tid = threadIdx.x;
@@ -372,8 +373,10 @@ prefix_quad_kernel(int layers, int entangler, const double* __restrict__ thetas,
     for (int r = 0; r < 4; ++r) {
       const double2 pp =
           make_double2(__shfl_xor_sync(full, v[r].x, 1 << lbit), __shfl_xor_sync(full, v[r].y, 1 << lbit));
+      // self part first (overlaps the shuffle latency), then two FMAs on the partner:
+      // 4 FP64 ops per component (DMUL + 3 DFMA), 2 of them after the shuffle
       const double sr = fma(cs.x, v[r].x, -cs.y * v[r].y), si = fma(cs.x, v[r].y, cs.y * v[r].x);
-      v[r] = make_double2(sr + fma(co.x, pp.x, -co.y * pp.y), si + fma(co.x, pp.y, co.y * pp.x));
+      v[r] = make_double2(fma(co.x, pp.x, fma(-co.y, pp.y, sr)), fma(co.x, pp.y, fma(co.y, pp.x, si)));
     }
   };
 
@@ -383,29 +386,32 @@ prefix_quad_kernel(int layers, int entangler, const double* __restrict__ thetas,
     reg_gate(gl + (n - 1 - 1), 1);
 #pragma unroll
     for (int pos = 2; pos < 7; ++pos) lane_gate(gl + (n - 1 - pos), pos - 2);
+    // Buffer discipline: a buffer is rewritten only after a barrier that follows every read of
+    // it (the reads of sbuf0 precede the barrier of sbuf1 and vice versa), so each transpose
+    // needs a single barrier.  W = 0 (no warp bits): alternate the one transpose per layer.
+    double2* ring = sbuf1;
     if (W > 0) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r) sbuf[qswz(iX0 | r)] = v[r];
+      for (int r = 0; r < 4; ++r) sbuf0[qswz(iX0 | r)] = v[r];
       __syncthreads();
 #pragma unroll
-      for (int r = 0; r < 4; ++r) v[r] = sbuf[qswz(iY0 | r)];
-      __syncthreads();
+      for (int r = 0; r < 4; ++r) v[r] = sbuf0[qswz(iY0 | r)];
 #pragma unroll
       for (int pos = 7; pos < n; ++pos) lane_gate(gl + (n - 1 - pos), pos - 7);
 #pragma unroll
-      for (int r = 0; r < 4; ++r) sbuf[qswz(iY0 | r)] = v[r];
+      for (int r = 0; r < 4; ++r) sbuf1[qswz(iY0 | r)] = v[r];
     } else {
+      ring = (layer & 1) ? sbuf1 : sbuf0;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) sbuf[qswz(iX0 | r)] = v[r];
+      for (int r = 0; r < 4; ++r) ring[qswz(iX0 | r)] = v[r];
     }
     __syncthreads();
     // entangling ring folded into the read back to layout X
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      const double2 a = sbuf[pX[r]];
+      const double2 a = ring[pX[r]];
       v[r] = nX[r] ? make_double2(-a.x, -a.y) : a;
     }
-    __syncthreads();
   }
   double2* x = x_all + (size_t)blockIdx.x * N;
 #pragma unroll

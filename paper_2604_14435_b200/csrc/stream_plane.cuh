@@ -1,0 +1,397 @@
+// stream_plane.cuh - the n >= 11, uniform-b Hadamard-test path on REAL planes.
+//
+// Same circuits, same passes and the same algorithmic work as stream_hadamard_kernel
+// (stream.cuh, whose tile geometry, layouts, column walks and prefetch it reuses), with the
+// branch split the way plane.cuh splits it at n = 10: for uniform b every gate after the first
+// ancilla H is a real matrix (signed permutations c-A_k / c-A_l, c-H^{(x)n}, c-Z_j), so Re(phi)
+// and Im(phi) evolve independently.  A CTA runs the whole pass sequence of one circuit twice,
+// once per plane, and adds the two readout halves:
+//     Re S = sum x'_re phi_re + sum x'_im phi_im,   Im S = sum x'_re phi_im - sum x'_im phi_re.
+// A thread holds 16 doubles (32 registers instead of 64), so 4 CTAs fit on an SM instead of 2
+// and their load / butterfly / exchange phases overlap; HBM bytes per circuit are unchanged
+// (each plane's scratch is half the complex one).  x is read from a planar copy
+// [x_re | x_im] (to_planar_kernel), so every x load uses whole sectors.
+//
+// SMEM: one tile of 2^TB doubles in rows padded to 17 (slot(e) = e + (e >> 4)): in every layout
+// (LL, LM, LH) a half-warp's 16 doubles hit 16 distinct 8-byte bank pairs and the address is a
+// per-lane base plus a compile-time immediate, issued as a shared-window access (no address
+// arithmetic per element).
+#pragma once
+
+#include "stream.cuh"
+
+namespace dvqls {
+namespace streamp {
+
+using stream::Cols;
+using stream::Geo;
+using stream::LL_;
+using stream::LM_;
+using stream::TS;
+
+// x_all (K thetas x 2^n complex, interleaved) -> xp (K x [re 2^n | im 2^n])
+__global__ void __launch_bounds__(256) to_planar_kernel(const double2* __restrict__ x, uint32_t N, uint32_t K,
+                                                        double* __restrict__ xp) {
+  const size_t total = size_t(N) * K;
+  for (size_t i = size_t(blockIdx.x) * 256 + threadIdx.x; i < total; i += size_t(gridDim.x) * 256) {
+    const size_t k = i / N, j = i - k * N;
+    const double2 a = x[i];
+    xp[2 * k * N + j] = a.x;
+    xp[(2 * k + 1) * N + j] = a.y;
+  }
+}
+
+__device__ __forceinline__ uint32_t sbase() { return uint32_t(__cvta_generic_to_shared(dvqls_smem)); }
+__device__ __forceinline__ double lds(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__host__ __device__ constexpr uint32_t pslot(uint32_t e) { return e + (e >> 4); }
+template <int TB>
+__host__ __device__ constexpr size_t tile_smem() {
+  return sizeof(double) * pslot(1u << TB);
+}
+
+// &base[idx] (8-byte elements) as one IMAD.WIDE.U32
+__device__ __forceinline__ const double* atd(const double* base, uint32_t idx) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, 8, %2;" : "=l"(r) : "r"(idx), "l"(base));
+  return reinterpret_cast<const double*>(r);
+}
+__device__ __forceinline__ double* atd(double* base, uint32_t idx) {
+  return const_cast<double*>(atd(const_cast<const double*>(base), idx));
+}
+
+// butterflies on register bit i for the tile bits of layout S in [lo, hi) (stream::stages, real)
+template <int S, int TB>
+__device__ __forceinline__ void stages(double (&v)[16], int lo, int hi) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int q = S + i;
+    if (S == TS<TB>::SH && q < 8) continue;  // TB = 11: bit 7 belongs to LM
+    if (q >= lo && q < hi) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (!(r & (1 << i))) {
+          const double p = v[r], w = v[r | (1 << i)];
+          v[r] = p + w;
+          v[r | (1 << i)] = p - w;
+        }
+    }
+  }
+}
+
+// layout SA -> SB through the padded tile buffer at shared-window address sm
+template <int SA, int SB>
+__device__ __forceinline__ void xchg(double (&v)[16], uint32_t sm, uint32_t t) {
+  const uint32_t a = sm + pslot(stream::lelem<SA>(t, 0)) * 8u, b = sm + pslot(stream::lelem<SB>(t, 0)) * 8u;
+  __syncthreads();  // previous readers of the buffer are done
+#pragma unroll
+  for (int r = 0; r < 16; ++r) sts(a + pslot(stream::lelem<SA>(0, uint32_t(r))) * 8u, v[r]);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = lds(b + pslot(stream::lelem<SB>(0, uint32_t(r))) * 8u);
+}
+
+// v_r = sgn_k(j_r ^ m) x_pl[j_r ^ m]   (c-A_k on one plane)
+template <int S>
+__device__ __forceinline__ void gather(double (&v)[16], const double* __restrict__ xpl, const Cols<S>& cc, uint32_t m,
+                                       uint32_t z) {
+  const uint32_t w = stream::sword(cc.parity_word(z), __popc((cc.jb ^ m) & z) & 1u);
+  uint32_t jj = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int r = k ^ (k >> 1);
+    jj = cc.step(jj, k);
+    v[r] = flip(__ldg(atd(xpl, jj ^ m)), stream::smask(w, r));
+  }
+}
+
+// this plane's half of Re S (xr = own plane) or Im S (xr = other plane, negated for the Re plane
+// through `neg`): sum_r sgn_l(j_r) xr[j_r ^ m] v_r
+template <int S>
+__device__ __forceinline__ double readout(const double (&v)[16], const double* __restrict__ xr, const Cols<S>& cc,
+                                          uint32_t m, uint32_t z, uint32_t neg) {
+  const uint32_t w = stream::sword(cc.parity_word(z), (__popc(cc.jb & z) & 1u) ^ neg);
+  double a0 = 0.0, a1 = 0.0;
+  uint32_t jj = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int r = k ^ (k >> 1);
+    jj = cc.step(jj, k);
+    const double a = flip(__ldg(atd(xr, jj ^ m)), stream::smask(w, r));
+    if (k & 1) a1 = fma(a, v[r], a1); else a0 = fma(a, v[r], a0);
+  }
+  return a0 + a1;
+}
+
+template <int S>
+__device__ __forceinline__ void zsign(double (&v)[16], const Cols<S>& cc, int p) {
+  const uint32_t w = stream::sword(cc.parity_word(1u << p), (cc.jb >> p) & 1u);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = flip(v[r], stream::smask(w, r));
+}
+
+template <int S>
+__device__ __forceinline__ void gload(double (&v)[16], const double* __restrict__ src, const Cols<S>& cc) {
+  uint32_t jj = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    jj = cc.step(jj, k);
+    v[k ^ (k >> 1)] = __ldcg(atd(src, jj));
+  }
+}
+
+template <int S>
+__device__ __forceinline__ void gstore(const double (&v)[16], double* __restrict__ dst, const Cols<S>& cc) {
+  uint32_t jj = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    jj = cc.step(jj, k);
+    __stcg(atd(dst, jj), v[k ^ (k >> 1)]);
+  }
+}
+
+// stream::prefetch_tile counts 16-byte amplitudes; a plane tile is half the bytes: prefetch the
+// same index ranges of a double array (the base pointer is reinterpreted; sizes halve)
+__device__ __forceinline__ void prefetch_tile_d(const double* __restrict__ base, const Geo& g, uint32_t tau,
+                                                uint32_t flip_hi, uint32_t t, uint32_t nthreads) {
+  if (g.b == g.c) {
+    const uint32_t chunk = (1u << g.tb) / 16u;
+    if (t < 16u) stream::prefetch_l2(base + ((g.gidx(t * chunk, tau)) ^ flip_hi), chunk * 8u);
+  } else {
+    const uint32_t runs = 1u << (g.tb - g.c);
+    for (uint32_t u = t; u < runs; u += nthreads)
+      stream::prefetch_l2(base + (g.gidx(u << g.c, tau) ^ flip_hi), 8u << g.c);
+  }
+}
+
+template <int TB, int C>
+__device__ __forceinline__ void mid_pass_c(double* __restrict__ phi, uint32_t sm, const Geo& g, int kind, int p,
+                                           uint32_t t0, uint32_t t1, uint32_t t) {
+  constexpr int lo = C, hi = TB, SH = TS<TB>::SH;
+  constexpr bool needLM = lo < 8, needLL = lo < 4;
+  for (uint32_t tau = t0; tau < t1; ++tau) {
+    if (tau + 1 < t1) prefetch_tile_d(phi, g, tau + 1, 0u, t, TS<TB>::THREADS);
+    double v[16];
+    if (!needLM) {
+      const Cols<SH> cc(g, t, tau);
+      gload(v, phi, cc);
+      stages<SH, TB>(v, lo, hi);
+      if (kind == 1) { zsign(v, cc, p); stages<SH, TB>(v, lo, hi); }
+      gstore(v, phi, cc);
+    } else if (kind == 2) {
+      const Cols<SH> ch(g, t, tau);
+      gload(v, phi, ch);
+      stages<SH, TB>(v, lo, hi);
+      if (needLL) {
+        xchg<SH, LL_>(v, sm, t);
+        stages<LL_, TB>(v, lo, hi);
+        xchg<LL_, LM_>(v, sm, t);
+      } else {
+        xchg<SH, LM_>(v, sm, t);
+      }
+      stages<LM_, TB>(v, lo, hi);
+      gstore(v, phi, Cols<LM_>(g, t, tau));
+    } else {
+      const Cols<LM_> cm(g, t, tau);
+      gload(v, phi, cm);
+      stages<LM_, TB>(v, lo, hi);
+      if (needLL) {
+        xchg<LM_, LL_>(v, sm, t);
+        stages<LL_, TB>(v, lo, hi);
+        xchg<LL_, SH>(v, sm, t);
+      } else {
+        xchg<LM_, SH>(v, sm, t);
+      }
+      stages<SH, TB>(v, lo, hi);
+      if (kind == 0) {
+        gstore(v, phi, Cols<SH>(g, t, tau));
+      } else {
+        zsign(v, Cols<SH>(g, t, tau), p);
+        stages<SH, TB>(v, lo, hi);
+        if (needLL) {
+          xchg<SH, LL_>(v, sm, t);
+          stages<LL_, TB>(v, lo, hi);
+          xchg<LL_, LM_>(v, sm, t);
+        } else {
+          xchg<SH, LM_>(v, sm, t);
+        }
+        stages<LM_, TB>(v, lo, hi);
+        gstore(v, phi, cm);
+      }
+    }
+  }
+}
+
+template <int TB>
+__device__ __forceinline__ void mid_pass(double* __restrict__ phi, uint32_t sm, const Geo& g, int kind, int p,
+                                         uint32_t t0, uint32_t t1, uint32_t t) {
+  switch (g.c) {
+    case 2: mid_pass_c<TB, 2>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 3: mid_pass_c<TB, 3>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 4: mid_pass_c<TB, 4>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 5: mid_pass_c<TB, 5>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 6: mid_pass_c<TB, 6>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 7: mid_pass_c<TB, 7>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 8: mid_pass_c<TB, 8>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 9: mid_pass_c<TB, 9>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 10: mid_pass_c<TB, 10>(phi, sm, g, kind, p, t0, t1, t); break;
+    default: mid_pass_c<TB, 11>(phi, sm, g, kind, p, t0, t1, t); break;
+  }
+}
+
+// P0: gather (c-A_k) + F1 on tile bits, store the plane's scratch
+template <int TB>
+__device__ __forceinline__ void first_pass(double* __restrict__ phi, const double* __restrict__ xpl, uint32_t sm,
+                                           const Geo& g0, const PauliTerm& Tk, bool big_x, uint32_t ntiles,
+                                           uint32_t t) {
+  constexpr int SH = TS<TB>::SH;
+  for (uint32_t tau = 0; tau < ntiles; ++tau) {
+    if (big_x && tau + 1 < ntiles)
+      prefetch_tile_d(xpl, g0, tau + 1, Tk.xm & ~uint32_t(TS<TB>::TN - 1), t, TS<TB>::THREADS);
+    double v[16];
+    gather(v, xpl, Cols<LM_>(g0, t, tau), Tk.xm, Tk.zm);
+    stages<LM_, TB>(v, 0, TB);
+    xchg<LM_, LL_>(v, sm, t);
+    stages<LL_, TB>(v, 0, TB);
+    xchg<LL_, SH>(v, sm, t);
+    stages<SH, TB>(v, 0, TB);
+    gstore(v, phi, Cols<SH>(g0, t, tau));
+  }
+}
+
+// last pass: F2 on tile bits + this plane's readout half
+template <int TB>
+__device__ __forceinline__ double last_pass(const double* __restrict__ phi, const double* __restrict__ xr, uint32_t sm,
+                                            const Geo& g0, const PauliTerm& Tl, uint32_t neg, bool big_x,
+                                            uint32_t ntiles, uint32_t t) {
+  constexpr int SH = TS<TB>::SH;
+  double acc = 0.0;
+  for (uint32_t tau = 0; tau < ntiles; ++tau) {
+    if (tau + 1 < ntiles) {
+      prefetch_tile_d(phi, g0, tau + 1, 0u, t, TS<TB>::THREADS);
+      if (big_x) prefetch_tile_d(xr, g0, tau + 1, Tl.xm & ~uint32_t(TS<TB>::TN - 1), t, TS<TB>::THREADS);
+    }
+    double v[16];
+    gload(v, phi, Cols<SH>(g0, t, tau));
+    stages<SH, TB>(v, 0, TB);
+    xchg<SH, LL_>(v, sm, t);
+    stages<LL_, TB>(v, 0, TB);
+    xchg<LL_, LM_>(v, sm, t);
+    stages<LM_, TB>(v, 0, TB);
+    acc += readout(v, xr, Cols<LM_>(g0, t, tau), Tl.xm, Tl.zm, neg);
+  }
+  return acc;
+}
+
+// a3-a9 for n >= 11, uniform b: one circuit per CTA at a time, Re plane then Im plane.
+// x_all: planar thetas [K][re 2^n | im 2^n];  scratch: 2^n doubles per CTA (n > TB).
+constexpr int MIN_CTAS = 3;  // CTAs per SM the register budget is sized for (80 registers)
+template <int TB>
+__global__ void __launch_bounds__(TS<TB>::THREADS, MIN_CTAS)
+stream_plane_kernel(const double* __restrict__ x_all, const PauliTerm* __restrict__ tab,
+                    const double2* __restrict__ coef, int L, int n, int64_t c0, int64_t C,
+                    const int64_t* __restrict__ cidx, double* __restrict__ scratch, double* __restrict__ out_terms,
+                    double* __restrict__ partials, int with_cost, double* __restrict__ red_out,
+                    unsigned* __restrict__ counter, P2PArgs p2p) {
+  using T = TS<TB>;
+  constexpr int SH = T::SH;
+  __shared__ double red[T::THREADS / 32];
+  __shared__ double acc4[4];
+  const uint32_t sm = sbase();
+  const int kth = blockIdx.y;
+  const uint32_t N = 1u << n;
+  const double* __restrict__ xre = x_all + (size_t)kth * 2 * N;
+  double* __restrict__ phi = scratch + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * N;  // n > TB only
+  const int ng = stream::ngroups(n, TB);
+  const uint32_t t = threadIdx.x;
+  const int64_t G = gridDim.x;
+  const int64_t cb = (int64_t)blockIdx.x * C / G, ce = ((int64_t)blockIdx.x + 1) * C / G;
+  const uint32_t ntiles = N > uint32_t(T::TN) ? N >> TB : 1u;
+  const Geo g0 = stream::group(n, 0, TB);
+  const bool big_x = n > 22;
+  if (t == 0) acc4[0] = acc4[1] = acc4[2] = acc4[3] = 0.0;
+
+  for (int64_t cl = cb; cl < ce; ++cl) {
+    const int64_t c = cidx ? cidx[cl] : c0 + cl;
+    const int64_t tk = c >> 1;
+    const int part = int(c & 1);
+    const int sidx = int(tk % (n + 1));
+    const int64_t lk = tk / (n + 1);
+    const int k = int(lk % L), l = int(lk / L);
+    const PauliTerm Tk = tab[k], Tl = tab[l];
+    const int q = (Tk.ny + Tl.ny + 3 * part) & 3;
+    const uint32_t im = uint32_t(q & 1);
+    const int p = n - 1 - (sidx - 1);  // Z_j bit position (numerators)
+    double acc = 0.0;
+#pragma unroll 1
+    for (uint32_t pl = 0; pl < 2; ++pl) {
+      const double* __restrict__ xpl = xre + size_t(pl) * N;       // gather plane
+      const double* __restrict__ xr = xre + size_t(pl ^ im) * N;   // readout plane
+      const uint32_t neg = im & (pl ^ 1u);                         // Re plane of Im S: minus
+      if (sidx == 0) {
+        for (uint32_t tau = 0; tau < ntiles; ++tau) {
+          const Cols<LM_> cm(g0, t, tau);
+          double v[16];
+          gather(v, xpl, cm, Tk.xm, Tk.zm);
+          acc += readout(v, xr, cm, Tl.xm, Tl.zm, neg);
+        }
+      } else if (n <= TB) {
+        const Cols<LM_> cm(g0, t, 0);
+        double v[16];
+        gather(v, xpl, cm, Tk.xm, Tk.zm);
+        stages<LM_, TB>(v, 0, TB);
+        xchg<LM_, LL_>(v, sm, t);
+        stages<LL_, TB>(v, 0, TB);
+        xchg<LL_, SH>(v, sm, t);
+        stages<SH, TB>(v, 0, TB);
+        zsign(v, Cols<SH>(g0, t, 0), p);
+        stages<SH, TB>(v, 0, TB);
+        xchg<SH, LL_>(v, sm, t);
+        stages<LL_, TB>(v, 0, TB);
+        xchg<LL_, LM_>(v, sm, t);
+        stages<LM_, TB>(v, 0, TB);
+        acc += readout(v, xr, cm, Tl.xm, Tl.zm, neg);
+      } else {
+        first_pass<TB>(phi, xpl, sm, g0, Tk, big_x, ntiles, t);
+        __syncthreads();
+        if (ng == 2) {
+          mid_pass<TB>(phi, sm, stream::group(n, 1, TB), 1, p, 0, ntiles, t);
+        } else {
+          mid_pass<TB>(phi, sm, stream::group(n, 1, TB), 0, p, 0, ntiles, t);
+          __syncthreads();
+          mid_pass<TB>(phi, sm, stream::group(n, 2, TB), 1, p, 0, ntiles, t);
+          __syncthreads();
+          mid_pass<TB>(phi, sm, stream::group(n, 1, TB), 2, p, 0, ntiles, t);
+        }
+        __syncthreads();
+        acc += last_pass<TB>(phi, xr, sm, g0, Tl, neg, big_x, ntiles, t);
+        __syncthreads();  // scratch reads done before the next plane's / circuit's P0
+      }
+    }
+    double val = stream::block_sum(acc, red, T::THREADS);
+    if (t == 0) {
+      if (sidx > 0) val *= 1.0 / double(N);   // two unnormalised FWHTs
+      val = (q == 1 || q == 2) ? -val : val;  // Re(i^q S)
+      out_terms[(size_t)kth * C + cl] = val;
+      const double2 cl_ = coef[l], ck = coef[k];
+      const double wr = cl_.x * ck.x + cl_.y * ck.y, wi = cl_.x * ck.y - cl_.y * ck.x;
+      const double cr = part == 0 ? wr * val : -wi * val;
+      const double ci = part == 0 ? wi * val : wr * val;
+      if (sidx == 0) { acc4[2] += cr; acc4[3] += ci; } else { acc4[0] += cr; acc4[1] += ci; }
+    }
+  }
+  if (t == 0) {
+    double* o = partials + ((size_t)kth * G + blockIdx.x) * 4;
+    o[0] = acc4[0]; o[1] = acc4[1]; o[2] = acc4[2]; o[3] = acc4[3];
+  }
+  if (red_out) finish_partials(partials, G, kth, n, with_cost, red_out, counter, p2p.world > 1 ? &p2p : nullptr);
+}
+
+}  // namespace streamp
+}  // namespace dvqls

@@ -117,3 +117,23 @@ def test_cfg5_n16_full_sampled(dv, team, monkeypatch):
     idx = np.linspace(0, w.n_circuits - 1, 24).astype(np.int64)
     idx[1::2] |= 1
     assert np.max(np.abs(g[idx] - sim.workload_terms(w, th, idx=idx))) <= TOL
+
+
+@pytest.mark.parametrize("n,L,ent", [(11, 3, 0), (12, 2, 1), (13, 2, 0), (14, 2, 0)])
+def test_complex_stream_kernel(dv, n, L, ent, monkeypatch):
+    """DVQLS_PLANE=0 keeps the complex-layout streaming kernel (uniform b) selectable: full terms
+    and a batch of two thetas against the oracle (the default above is the real-plane kernel)."""
+    monkeypatch.setenv("DVQLS_PLANE", "0")
+    w = configs.random_workload(n, L, 2, seed=90 + n, entangler=ent)
+    ctx = dv.from_workload(w, max_batch=2)
+    try:
+        th = w.theta0()
+        g = ctx.terms(th)
+        ths = np.stack([w.theta0(s) for s in range(2)])
+        cb, _ = ctx.cost_batch(ths)
+    finally:
+        ctx.destroy()
+    assert np.max(np.abs(g - sim.workload_terms(w, th))) <= TOL
+    for k in range(2):
+        rk = sim.workload_terms(w, ths[k])
+        assert abs(cb[k] - ocost.cost(rk, ocost.coeffs_of(w), w.n, w.L)[0]) <= TOL

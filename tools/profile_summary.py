@@ -52,10 +52,11 @@ def launches(path):
             elif r[ui] in ("msecond", "ms"):
                 v *= 1e6
             d[re.sub(r"\(.*", "", r[ki])[:70]].append(v)
-    tot = sum(sum(v) for k, v in d.items() if "dvqls" in k)
+    ours = re.compile(r"dvqls|plane::|streamp::|stream::|pauli::|decomp::|glob::|tile::")
+    tot = sum(sum(v) for k, v in d.items() if ours.search(k))
     print(f"{'kernel':70s} {'launches':>8s} {'mean us':>10s} {'share of dvqls time':>20s}")
     for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
-        share = f"{100 * sum(v) / tot:.1f}%" if "dvqls" in k else "-"
+        share = f"{100 * sum(v) / tot:.1f}%" if ours.search(k) else "-"
         print(f"{k:70s} {len(v):8d} {sum(v) / len(v) / 1e3:10.2f} {share:>20s}")
 
 
