@@ -28,30 +28,43 @@ namespace dvqls {
 namespace decomp {
 
 constexpr int THREADS = 512;
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 constexpr int SORT_MAX = 4096;
 constexpr size_t SORT_SMEM = SORT_MAX * (8 + 8 + 4);
 
 // XOR-diagonal transposition B[m, k] = A[k, k ^ m] in 32 x 32 tiles: the tile of rows
 // [k0, k0+32) x columns [j0, j0+32) holds exactly the elements of B rows M0 + (a ^ b) (M0 =
 // (k0 ^ j0) & ~31), columns k0 + a; read along j and written along k, both coalesced.
-// fro[tile] = sum of |A|^2 over the tile (fixed order), for the Parseval candidate bound.
+// Persistent over the 32 x 32 tiles; fro[cta] = sum of |A|^2 over the CTA's tiles (fixed order),
+// for the Parseval candidate bound.
 __global__ void __launch_bounds__(256) xor_transpose_kernel(const double2* __restrict__ A, int n,
                                                             double2* __restrict__ B, double* __restrict__ fro) {
   __shared__ double2 t[32][33];
   __shared__ double red[8];
   const uint32_t N = 1u << n, tiles = N >> 5;
-  const uint32_t k0 = (blockIdx.x / tiles) << 5, j0 = (blockIdx.x % tiles) << 5;
   const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   double acc = 0.0;
-  for (uint32_t r = ty; r < 32; r += 8) {
-    const double2 a = __ldcs(A + size_t(k0 + r) * N + j0 + tx);
-    acc = fma(a.x, a.x, fma(a.y, a.y, acc));
-    t[r][tx] = a;
+  for (uint32_t tile = blockIdx.x; tile < tiles * tiles; tile += gridDim.x) {  // persistent
+    const uint32_t k0 = (tile / tiles) << 5, j0 = (tile % tiles) << 5;
+    {  // bulk-prefetch the next tile's 32 row segments (512 B each) into L2
+      const uint32_t nt = tile + gridDim.x;
+      if (nt < tiles * tiles && threadIdx.x < 32)
+        prefetch_l2(A + size_t(((nt / tiles) << 5) + threadIdx.x) * N + ((nt % tiles) << 5), 512u);
+    }
+    __syncthreads();  // previous tile's readers of t are done
+    for (uint32_t r = ty; r < 32; r += 8) {
+      const double2 a = __ldcs(A + size_t(k0 + r) * N + j0 + tx);
+      acc = fma(a.x, a.x, fma(a.y, a.y, acc));
+      t[r][tx] = a;
+    }
+    __syncthreads();
+    const uint32_t M0 = (k0 ^ j0) & ~31u;
+    for (uint32_t ml = ty; ml < 32; ml += 8)  // row M0 + ml of B gets A[k0 + tx, j0 + (tx ^ ml)]
+      B[size_t(M0 + ml) * N + k0 + tx] = t[tx][tx ^ ml];
   }
-  __syncthreads();
-  const uint32_t M0 = (k0 ^ j0) & ~31u;
-  for (uint32_t ml = ty; ml < 32; ml += 8)  // row M0 + ml of B gets A[k0 + tx, j0 + (tx ^ ml)]
-    B[size_t(M0 + ml) * N + k0 + tx] = t[tx][tx ^ ml];
   for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (tx == 0) red[ty] = acc;
   __syncthreads();
@@ -78,9 +91,10 @@ __global__ void __launch_bounds__(256) fro_small_kernel(const double2* __restric
 }
 
 // candidate threshold from Parseval: thr0 = eps * sqrt(sum fro / 2^n) * (1 - 1e-9) (below the
-// exact eps ||c||_2 by far more than the rounding gap), floor 1e-14; zeroes the candidate counter
+// exact eps ||c||_2 by far more than the rounding gap), floor 1e-14, stored as the bound on the
+// unscaled FWHT value f = 2^n c:  *thrf2 = (2^n thr0)^2;  zeroes the candidate counter
 __global__ void __launch_bounds__(256) prenorm_kernel(const double* __restrict__ fro, uint32_t nf, uint32_t N,
-                                                      double eps, double* __restrict__ thr0,
+                                                      double eps, double* __restrict__ thrf2,
                                                       unsigned long long* __restrict__ count) {
   __shared__ double red[256];
   double a = 0.0;
@@ -92,25 +106,29 @@ __global__ void __launch_bounds__(256) prenorm_kernel(const double* __restrict__
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    *thr0 = fmax(1e-14, eps * sqrt(red[0] / double(N)) * (1.0 - 1e-9));
+    const double thr0 = fmax(1e-14, eps * sqrt(red[0] / double(N)) * (1.0 - 1e-9));
+    *thrf2 = (thr0 * double(N)) * (thr0 * double(N));
     *count = 0ull;
   }
 }
 
 // Epilogue of one coefficient c = i^{popcount(m&z)} f / 2^n (f = FWHT value):
-// MODE 0 writes C[m, z];  MODE 1 compacts candidates |c| >= *thr0 into (idx, C[slot]) and returns
-// |c|^2 for the row's fixed-order sum.
+// MODE 0 writes C[m, z];  MODE 1 compacts candidates |f|^2 >= thrf2 (i.e. |c| >= thr0) into
+// (idx, C[slot]) and returns |f|^2 for the row's fixed-order sum (scaled by 4^-n once per row:
+// a power of two, so sum |c|^2 is exact to the same rounding).  No square root or phase work on
+// the common (non-candidate) path.
 template <int MODE>
-__device__ __forceinline__ double emit_coef(double2 f, uint32_t m, uint32_t z, uint32_t N, double inv, double thr,
+__device__ __forceinline__ double emit_coef(double2 f, uint32_t m, uint32_t z, uint32_t N, double inv, double thrf2,
                                             double2* __restrict__ C, uint64_t cap,
                                             unsigned long long* __restrict__ count, uint64_t* __restrict__ idx) {
-  const int q = __popc(m & z) & 3;  // i^q
-  const double re = (q == 0 ? f.x : q == 1 ? -f.y : q == 2 ? -f.x : f.y) * inv;
-  const double im = (q == 0 ? f.y : q == 1 ? f.x : q == 2 ? -f.y : -f.x) * inv;
-  if (MODE == 0) C[size_t(m) * N + z] = make_double2(re, im);
-  if (MODE == 1) {
-    const double a = sqrt(fma(re, re, im * im));
-    if (a >= thr) {
+  const double a2 = fma(f.x, f.x, f.y * f.y);
+  if (MODE == 0 || a2 >= thrf2) {
+    const int q = __popc(m & z) & 3;  // i^q
+    const double re = (q == 0 ? f.x : q == 1 ? -f.y : q == 2 ? -f.x : f.y) * inv;
+    const double im = (q == 0 ? f.y : q == 1 ? f.x : q == 2 ? -f.y : -f.x) * inv;
+    if (MODE == 0) {
+      C[size_t(m) * N + z] = make_double2(re, im);
+    } else {
       const unsigned long long slot = atomicAdd(count, 1ull);
       if (slot < cap) {
         idx[slot] = uint64_t(m) * N + z;
@@ -118,12 +136,12 @@ __device__ __forceinline__ double emit_coef(double2 f, uint32_t m, uint32_t z, u
       }
     }
   }
-  return fma(re, re, im * im);
+  return a2;
 }
 
-// CTA sum of per-thread |c|^2 partials in a fixed order -> sq[blockIdx.x]
+// CTA sum of per-thread |f|^2 partials in a fixed order, times 4^-n -> sq[m] = sum_z |c_(m,z)|^2
 template <int NT>
-__device__ __forceinline__ void row_sq(double acc, double* __restrict__ sq) {
+__device__ __forceinline__ void row_sq(double acc, double* __restrict__ sq, double inv, uint32_t m) {
   __shared__ double red[NT / 32];
   for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
@@ -131,7 +149,7 @@ __device__ __forceinline__ void row_sq(double acc, double* __restrict__ sq) {
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < NT / 32; ++w) t += red[w];  // fixed order
-    sq[blockIdx.x] = t;
+    sq[m] = t * (inv * inv);
   }
 }
 
@@ -139,7 +157,7 @@ __device__ __forceinline__ void row_sq(double acc, double* __restrict__ sq) {
 template <int MODE>
 __global__ void __launch_bounds__(THREADS)
 fwht_rows_kernel(const double2* __restrict__ B, int n, double2* __restrict__ C, double* __restrict__ sq,
-                 const double* __restrict__ thr0, uint64_t cap, unsigned long long* __restrict__ count,
+                 const double* __restrict__ thrf2, uint64_t cap, unsigned long long* __restrict__ count,
                  uint64_t* __restrict__ idx, int direct) {
   extern __shared__ double2 rows_smem[];  // dynamic: 2^n amplitudes
   __shared__ double red[THREADS / 32];
@@ -162,11 +180,11 @@ fwht_rows_kernel(const double2* __restrict__ B, int n, double2* __restrict__ C, 
     __syncthreads();
   }
   const double inv = 1.0 / double(N);
-  const double thr = MODE == 1 ? *thr0 : 0.0;
+  const double thr = MODE == 1 ? *thrf2 : 0.0;
   double acc = 0.0;
   for (uint32_t z = threadIdx.x; z < N; z += THREADS)
     acc += emit_coef<MODE>(rows_smem[z], m0, z, N, inv, thr, C, cap, count, idx);
-  if (MODE == 1) row_sq<THREADS>(acc, sq);
+  if (MODE == 1) row_sq<THREADS>(acc, sq, inv, blockIdx.x);
 }
 
 // n = NB >= 9: row m of B in registers, RG = 16 amplitudes per thread (2^(NB-4) threads).
@@ -182,17 +200,17 @@ __device__ __forceinline__ uint32_t rows_idx(uint32_t t, uint32_t r, int b) {
 __device__ __forceinline__ uint32_t rows_slot(uint32_t i) { return i ^ ((i >> 4) & 7u); }
 
 template <int NB, int MODE>
-__global__ void __launch_bounds__(1 << (NB - 4))
+__global__ void __launch_bounds__(1 << (NB - 4), NB <= 12 ? 3 : 1)
 fwht_rows_reg_kernel(const double2* __restrict__ B, double2* __restrict__ C, double* __restrict__ sq,
-                     const double* __restrict__ thr0, uint64_t cap, unsigned long long* __restrict__ count,
+                     const double* __restrict__ thrf2, uint64_t cap, unsigned long long* __restrict__ count,
                      uint64_t* __restrict__ idx) {
   static_assert(NB >= 9 && NB <= 13, "register FWHT rows: 9 <= n <= 13");
   constexpr int NT = 1 << (NB - 4);
   constexpr uint32_t N = 1u << NB;
   constexpr int NPASS = (NB + 3) / 4;
   extern __shared__ double2 rows_smem[];
-  const uint32_t t = threadIdx.x, m0 = blockIdx.x;
-  double2 v[RG];
+  const uint32_t t = threadIdx.x, m0 = blockIdx.x;  // one row per CTA (a persistent variant with
+  double2 v[RG];                                     // an L2 prefetch of the next row measured slower)
   const double2* row = B + size_t(m0) * N;
 #pragma unroll
   for (int r = 0; r < RG; ++r) v[r] = __ldcs(row + rows_idx<NB>(t, uint32_t(r), NB - 4));
@@ -222,26 +240,12 @@ fwht_rows_reg_kernel(const double2* __restrict__ B, double2* __restrict__ C, dou
     }
   }
   const double inv = 1.0 / double(N);
-  const double thr = MODE == 1 ? *thr0 : 0.0;
+  const double thr = MODE == 1 ? *thrf2 : 0.0;
   double acc = 0.0;
 #pragma unroll
   for (int r = 0; r < RG; ++r)
     acc += emit_coef<MODE>(v[r], m0, rows_idx<NB>(t, uint32_t(r), 0), N, inv, thr, C, cap, count, idx);
-  if (MODE == 1) row_sq<NT>(acc, sq);
-}
-
-// ||c||_2 = sqrt(sum_m sq[m]) in a fixed order (one CTA)
-__global__ void __launch_bounds__(THREADS) norm_kernel(const double* __restrict__ sq, uint32_t N, double* norm) {
-  __shared__ double red[THREADS];
-  double a = 0.0;
-  for (uint32_t i = threadIdx.x; i < N; i += THREADS) a += sq[i];
-  red[threadIdx.x] = a;
-  __syncthreads();
-  for (int off = THREADS / 2; off >= 1; off >>= 1) {
-    if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *norm = sqrt(red[0]);
+  if (MODE == 1) row_sq<NT>(acc, sq, inv, m0);
 }
 
 // lexicographic code of P(m, z): 2 bits per qubit from qubit 0 (MSB), I=0 X=1 Y=2 Z=3
@@ -260,18 +264,34 @@ __device__ __forceinline__ uint64_t lex_code(uint32_t m, uint32_t z, int n) {
 // Pauli strings (n chars each) in that order and the survivor count *out_L
 __global__ void __launch_bounds__(THREADS)
 sort_emit_kernel(const double2* __restrict__ C, int n, const uint64_t* __restrict__ idx,
-                 const unsigned long long* __restrict__ count, const double* __restrict__ norm, double eps,
-                 double2* __restrict__ out_c, char* __restrict__ out_s, unsigned long long* __restrict__ out_L) {
+                 const unsigned long long* __restrict__ count, const double* __restrict__ sq,
+                 double* __restrict__ norm, double eps, double2* __restrict__ out_c, char* __restrict__ out_s,
+                 unsigned long long* __restrict__ out_L) {
   extern __shared__ uint64_t sort_smem[];  // dynamic: SORT_MAX * 20 B
   uint64_t* kq = sort_smem;
   uint64_t* kl = sort_smem + SORT_MAX;
   uint32_t* ki = reinterpret_cast<uint32_t*>(sort_smem + 2 * SORT_MAX);
+  {  // ||c||_2 = sqrt(sum_m sq[m]) in a fixed order (strided partials, then a tree); SMEM reused below
+    double* red = reinterpret_cast<double*>(sort_smem);
+    double a = 0.0;
+    for (uint32_t i = threadIdx.x; i < (1u << n); i += THREADS) a += sq[i];
+    red[threadIdx.x] = a;
+    __syncthreads();
+    for (int off = THREADS / 2; off >= 1; off >>= 1) {
+      if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) *norm = sqrt(red[0]);
+    __syncthreads();
+  }
   const uint32_t L = uint32_t(min(*count, (unsigned long long)SORT_MAX));  // candidates
   uint32_t P = 1;
   while (P < L) P <<= 1;
   const uint32_t N = 1u << n;
-  const double q = 1e-12 * *norm;
-  const double thr = fmax(1e-14, eps * *norm);  // the pruning rule with the exact ||c||_2
+  __threadfence_block();
+  const double nrm = *norm;
+  const double q = 1e-12 * nrm;
+  const double thr = fmax(1e-14, eps * nrm);  // the pruning rule with the exact ||c||_2
   int kept = 0;
   for (uint32_t i = threadIdx.x; i < P; i += THREADS) {
     const double2 c = i < L ? C[i] : make_double2(0.0, 0.0);

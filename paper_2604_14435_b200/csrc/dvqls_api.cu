@@ -1126,7 +1126,8 @@ int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, boo
   if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10)
     return decomp_fail(DVQLS_E_CUDA, "libdvqls is built for sm_100a only");
   const size_t N = size_t(1) << n, NN = N * N;
-  const size_t nfro = n >= 5 ? (N >> 5) * (N >> 5) : 1;
+  // transposition CTAs (persistent over the (N/32)^2 tiles; one |A|^2 partial each)
+  const size_t nfro = n >= 5 ? std::min<size_t>((N >> 5) * (N >> 5), size_t(prop.multiProcessorCount) * 8) : 1;
   const uint64_t cap = decomp::SORT_MAX;
   if (cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking) || cudaMalloc((void**)&b.A, sizeof(double2) * NN) ||
       cudaMalloc((void**)&b.C, sizeof(double2) * (write_c ? NN : size_t(cap))) ||
@@ -1143,7 +1144,7 @@ int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, boo
   if (n >= 5 && cudaMalloc((void**)&b.B, sizeof(double2) * NN)) return decomp_fail(DVQLS_E_CUDA, "cudaMalloc B");
   if (ev0 && (cudaEventCreate(ev0) || cudaEventRecord(*ev0, b.st))) return decomp_fail(DVQLS_E_CUDA, "event");
   if (n >= 5)
-    decomp::xor_transpose_kernel<<<unsigned(nfro), 256, 0, b.st>>>(b.A, n, b.B, b.fro);
+    decomp::xor_transpose_kernel<<<unsigned(nfro), 256, 0, b.st>>>(b.A, n, b.B, b.fro);  // persistent
   else
     decomp::fro_small_kernel<<<1, 256, 0, b.st>>>(b.A, uint32_t(NN), b.fro);
   int rc;
@@ -1151,8 +1152,7 @@ int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, boo
     rc = launch_rows<0>(b, n, 0);
   } else {
     decomp::prenorm_kernel<<<1, 256, 0, b.st>>>(b.fro, uint32_t(nfro), uint32_t(N), eps, b.thr0, b.count);
-    rc = launch_rows<1>(b, n, cap);
-    if (!rc) decomp::norm_kernel<<<1, decomp::THREADS, 0, b.st>>>(b.sq, uint32_t(N), b.norm);
+    rc = launch_rows<1>(b, n, cap);  // the exact norm is formed inside sort_emit_kernel
   }
   if (rc) return rc;
   if (cudaGetLastError()) return decomp_fail(DVQLS_E_CUDA, "decomposition kernel launch failed");
@@ -1188,8 +1188,8 @@ int dvqls_decompose(int n, const double* A, double eps, int64_t max_terms, char*
   if (cudaFuncSetAttribute((const void*)&decomp::sort_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(decomp::SORT_SMEM)))
     return decomp_fail(DVQLS_E_CUDA, "sort kernel smem");
-  decomp::sort_emit_kernel<<<1, decomp::THREADS, decomp::SORT_SMEM, b.st>>>(b.C, n, b.idx, b.count, b.norm, eps,
-                                                                             b.oc, b.os, b.outL);
+  decomp::sort_emit_kernel<<<1, decomp::THREADS, decomp::SORT_SMEM, b.st>>>(b.C, n, b.idx, b.count, b.sq, b.norm,
+                                                                             eps, b.oc, b.os, b.outL);
   if (out_ms && (cudaEventCreate(&e1) || cudaEventRecord(e1, b.st)))
     return decomp_fail(DVQLS_E_CUDA, "event");
   unsigned long long cand = 0, L = 0;
