@@ -322,9 +322,13 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     KT = args.batch
     chars, co = w.arrays()
+    # device memory comes from torch: the library carves its tables from this workspace
+    ws_bytes = dvqls.workspace_size(w.n, w.layers, w.L, device=local, rank=rank, world=world,
+                                    max_batch=max(KT, 1))
+    workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     ctx = dvqls.Context(w.n, w.layers, chars, co, w.bkind, w.b, device=local, rank=rank, world=world,
                         nccl_id=nccl_id, entangler=w.entangler, stream=stream, timing=True,
-                        max_batch=max(KT, 1))
+                        max_batch=max(KT, 1), workspace=workspace)
     c0, c1 = ctx.local_range()
     thetas = np.stack([w.theta0(s) for s in range(KT)])
     th_dev = torch.tensor(thetas, dtype=torch.float64, device=dev)

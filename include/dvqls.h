@@ -86,13 +86,30 @@ typedef struct dvqls_opts {
   int timing;                  /* nonzero: record CUDA events around each kernel         */
   int max_batch;               /* largest K accepted by the *_batch calls (default 16)   */
   int mode;                    /* DVQLS_MODE_CIRCUITS (0, default) or DVQLS_MODE_PAULI   */
+  void* workspace_dev;         /* NULL: the library cudaMallocs its device tables once, in
+                                  dvqls_create.  Else: caller-owned device memory (e.g. a
+                                  torch tensor) of workspace_bytes >= dvqls_workspace_size(),
+                                  256-byte aligned; every per-context device buffer is carved
+                                  from it (the IPC-shared 4-double-per-theta allreduce buffer
+                                  of world > 1 is the one exception: IPC needs its own
+                                  allocation).  It must outlive the context.               */
+  size_t workspace_bytes;      /* size of workspace_dev                                   */
 } dvqls_opts;
 
 typedef struct dvqls_ctx dvqls_ctx;
 
+/* Device bytes a context with these parameters carves from opts->workspace_dev (SURVEY §8(b):
+ * the workspace is allocated by the caller, e.g. torch, so the library does no cudaMalloc
+ * for its tables).  Same rules as dvqls_create for n, layers, n_terms and opts (rank, world,
+ * max_batch, mode, device); for DVQLS_MODE_PAULI the bound assumes every task has its own
+ * observable.  Needs the device (kernel occupancy decides grid-sized buffers).  Returns 0 on
+ * invalid arguments or without a usable device. */
+size_t dvqls_workspace_size(int n_qubits, int layers, int n_terms, const dvqls_opts* opts);
+
 /* Build a context: parse the L Pauli strings into
  * (x_mask, z_mask, n_Y), copy coefficients, build U_b data, allocate device
- * buffers (the only cudaMalloc calls of the library), pick this rank's
+ * buffers (the only cudaMalloc calls of the library; none when opts->workspace_dev
+ * supplies the memory, see dvqls_workspace_size), pick this rank's
  * contiguous circuit block [c0, c1) = [rank*C/world, (rank+1)*C/world) of the
  * C = 2(n+1)L^2 circuits ("strided workload allocation"; a contiguous
  * block balances equally) and, for world > 1, create the NCCL

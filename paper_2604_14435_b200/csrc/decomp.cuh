@@ -160,7 +160,6 @@ fwht_rows_kernel(const double2* __restrict__ B, int n, double2* __restrict__ C, 
                  const double* __restrict__ thrf2, uint64_t cap, unsigned long long* __restrict__ count,
                  uint64_t* __restrict__ idx, int direct) {
   extern __shared__ double2 rows_smem[];  // dynamic: 2^n amplitudes
-  __shared__ double red[THREADS / 32];
   constexpr int NV = 1;
   const uint32_t N = 1u << n;
   const uint32_t m0 = blockIdx.x;

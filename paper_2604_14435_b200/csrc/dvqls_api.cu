@@ -174,6 +174,7 @@ struct dvqls_ctx {
   double2* d_scratch = nullptr;  // grid * N (n > 12; doubles when pstream)
   bool pstream = false;          // n >= 11, uniform b: real-plane streaming kernel (stream_plane.cuh)
   double* d_xp = nullptr;        // planar copy of x for pstream: [K][re N | im N]
+  std::vector<void**> carved;    // device buffers carved from a caller workspace (not freed)
   double2* d_x2 = nullptr;       // ring ping-pong buffer (n > 12 prefix)
   double2* d_gates = nullptr;    // fused-gate table (n > 12 prefix)
   int64_t* d_cidx = nullptr;     // circuit subset (dvqls_terms_subset)
@@ -393,6 +394,7 @@ int launch_eval(dvqls_ctx* ctx, int K, const double* thetas_dev, bool want_cost,
 
 void release(dvqls_ctx* c) {
   if (!c) return;
+  for (void** p : c->carved) *p = nullptr;  // owned by the caller's workspace
   for (int q = 0; q < int(c->peer_ptrs.size()); ++q)
     if (q != c->rank && c->peer_ptrs[q]) cudaIpcCloseMemHandle(c->peer_ptrs[q]);
   cudaFree(c->d_sym); cudaFree(c->d_peers);
@@ -467,10 +469,12 @@ int setup_p2p(dvqls_ctx* ctx) {
   return DVQLS_OK;
 }
 
-extern "C" {
-
-int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, const double* coeffs,
-                 const dvqls_bprep* bprep, const dvqls_opts* opts) {
+namespace {
+// dvqls_create, or (plan_bytes != NULL) only the planning part of it: everything up to the
+// device allocations runs as in a real create, then the total workspace size is returned and the
+// context is released (dvqls_workspace_size).
+int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, const double* coeffs,
+                const dvqls_bprep* bprep, const dvqls_opts* opts, size_t* plan_bytes) {
   g_create_err.clear();
   dvqls_ctx* ctx = nullptr;
   auto early = [&](int code, const char* msg) {
@@ -518,7 +522,7 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
     fail(ctx, DVQLS_E_ARG, "entangler must be 0 (CNOT ring) or 1 (CZ ring)");
     return bail(DVQLS_E_ARG);
   }
-  if (ctx->world > 1 && !(opts && opts->nccl_unique_id)) {
+  if (ctx->world > 1 && !plan_bytes && !(opts && opts->nccl_unique_id)) {
     fail(ctx, DVQLS_E_ARG, "world > 1 requires opts.nccl_unique_id");
     return bail(DVQLS_E_ARG);
   }
@@ -799,38 +803,69 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
     cudaGetLastError();
   }
 
-  // ---- device buffers (the library's only allocations) -----------------------
+  // ---- device buffers: cudaMalloc'd once here, or carved from the caller's workspace -----
   const int KB = ctx->max_batch;
-  auto alloc = [&](void** p, size_t bytes) { return cudaMalloc(p, bytes > 0 ? bytes : 16); };
-  if (alloc((void**)&ctx->d_tab, sizeof(PauliTerm) * L) || alloc((void**)&ctx->d_coef, sizeof(double2) * L) ||
-      alloc((void**)&ctx->d_hv, sizeof(double2) * ctx->N) ||
-      alloc((void**)&ctx->d_theta, sizeof(double) * KB * ctx->P) ||
-      alloc((void**)&ctx->d_x, sizeof(double2) * KB * ctx->N) ||
-      alloc((void**)&ctx->d_terms, sizeof(double) * KB * ctx->chunk) ||
-      alloc((void**)&ctx->d_partials, sizeof(double) * KB * ctx->NG * 4) ||
-      alloc((void**)&ctx->d_ep, sizeof(double) * KB * 4) || alloc((void**)&ctx->d_out, sizeof(double) * KB * 5) ||
-      (ctx->world > 1 && alloc((void**)&ctx->d_gather, sizeof(double) * ctx->world * ctx->chunk)) ||
-      alloc((void**)&ctx->d_counter, sizeof(unsigned) * KB) ||
-      alloc((void**)&ctx->d_gcounter, sizeof(unsigned) * KB) ||
-      alloc((void**)&ctx->d_beta, sizeof(double) * 2 * KB * size_t(L)) ||
-      alloc((void**)&ctx->d_out6, sizeof(double) * 6 * KB) ||
-      (ctx->bkind == DVQLS_B_AMPLITUDES && alloc((void**)&ctx->d_b, sizeof(double2) * ctx->N)) ||
-      (n > 12 && ctx->mode == DVQLS_MODE_CIRCUITS &&
-       alloc((void**)&ctx->d_scratch, (ctx->pstream ? sizeof(double) : sizeof(double2)) *
-                                           size_t(ctx->team ? ctx->nteams : ctx->grid) * ctx->N)) ||
-      (ctx->pstream && alloc((void**)&ctx->d_xp, sizeof(double2) * KB * ctx->N)) ||
-      (ctx->team && (alloc((void**)&ctx->d_team_acc, sizeof(double) * 2 * size_t(ctx->nteams) * ctx->team) ||
-                     alloc((void**)&ctx->d_team_ctr, sizeof(unsigned) * (size_t(ctx->nteams) + 1)))) ||
-      (ctx->mode == DVQLS_MODE_PAULI &&
-       (alloc((void**)&ctx->d_obs, sizeof(pauli::Obs) * obs.size()) ||
-        alloc((void**)&ctx->d_wE, sizeof(double2) * obs.size()) ||
-        alloc((void**)&ctx->d_wP, sizeof(double2) * obs.size()) ||
-        alloc((void**)&ctx->d_task, sizeof(uint32_t) * task.size()) ||
-        alloc((void**)&ctx->d_e, sizeof(double2) * obs.size()))) ||
-      (n > 12 && alloc((void**)&ctx->d_x2, sizeof(double2) * size_t(ctx->N))) ||
-      (n > 12 && alloc((void**)&ctx->d_gates, sizeof(double2) * 2 * size_t(n) * layers))) {
-    fail(ctx, DVQLS_E_CUDA, "cudaMalloc failed");
-    return bail(DVQLS_E_CUDA);
+  std::vector<std::pair<void**, size_t>> req;
+  auto buffer = [&](bool cond, void* p, size_t bytes) {
+    if (cond) req.emplace_back(reinterpret_cast<void**>(p), std::max<size_t>(bytes, 16));
+  };
+  // Pauli mode: a plan has no strings, so it sizes for one observable per task (the bound)
+  const size_t nobs = plan_bytes ? size_t(ctx->C / 2) : obs.size();
+  const size_t ntask = plan_bytes ? size_t(ctx->C / 2) : task.size();
+  buffer(true, &ctx->d_tab, sizeof(PauliTerm) * L);
+  buffer(true, &ctx->d_coef, sizeof(double2) * L);
+  buffer(true, &ctx->d_hv, sizeof(double2) * ctx->N);
+  buffer(true, &ctx->d_theta, sizeof(double) * KB * ctx->P);
+  buffer(true, &ctx->d_x, sizeof(double2) * KB * ctx->N);
+  buffer(true, &ctx->d_terms, sizeof(double) * KB * ctx->chunk);
+  buffer(true, &ctx->d_partials, sizeof(double) * KB * ctx->NG * 4);
+  buffer(true, &ctx->d_ep, sizeof(double) * KB * 4);
+  buffer(true, &ctx->d_out, sizeof(double) * KB * 5);
+  buffer(ctx->world > 1, &ctx->d_gather, sizeof(double) * ctx->world * ctx->chunk);
+  buffer(true, &ctx->d_counter, sizeof(unsigned) * KB);
+  buffer(true, &ctx->d_gcounter, sizeof(unsigned) * KB);
+  buffer(true, &ctx->d_beta, sizeof(double) * 2 * KB * size_t(L));
+  buffer(true, &ctx->d_out6, sizeof(double) * 6 * KB);
+  buffer(ctx->bkind == DVQLS_B_AMPLITUDES, &ctx->d_b, sizeof(double2) * ctx->N);
+  buffer(n > 12 && ctx->mode == DVQLS_MODE_CIRCUITS, &ctx->d_scratch,
+       (ctx->pstream ? sizeof(double) : sizeof(double2)) * size_t(ctx->team ? ctx->nteams : ctx->grid) * ctx->N);
+  buffer(ctx->pstream, &ctx->d_xp, sizeof(double2) * KB * ctx->N);
+  buffer(ctx->team, &ctx->d_team_acc, sizeof(double) * 2 * size_t(ctx->nteams) * ctx->team);
+  buffer(ctx->team, &ctx->d_team_ctr, sizeof(unsigned) * (size_t(ctx->nteams) + 1));
+  const bool pm = ctx->mode == DVQLS_MODE_PAULI;
+  buffer(pm, &ctx->d_obs, sizeof(pauli::Obs) * nobs);
+  buffer(pm, &ctx->d_wE, sizeof(double2) * nobs);
+  buffer(pm, &ctx->d_wP, sizeof(double2) * nobs);
+  buffer(pm, &ctx->d_task, sizeof(uint32_t) * ntask);
+  buffer(pm, &ctx->d_e, sizeof(double2) * nobs);
+  buffer(n > 12, &ctx->d_x2, sizeof(double2) * size_t(ctx->N));
+  buffer(n > 12, &ctx->d_gates, sizeof(double2) * 2 * size_t(n) * layers);
+  size_t total = 0;
+  for (auto& r : req) total += (r.second + 255) & ~size_t(255);
+  if (plan_bytes) {
+    *plan_bytes = total;
+    release(ctx);
+    delete ctx;
+    return DVQLS_OK;
+  }
+  if (opts && opts->workspace_dev) {
+    if ((reinterpret_cast<uintptr_t>(opts->workspace_dev) & 255u) || opts->workspace_bytes < total) {
+      fail(ctx, DVQLS_E_ARG, "workspace: %zu bytes at %p, need %zu bytes 256-byte aligned", opts->workspace_bytes,
+           opts->workspace_dev, total);
+      return bail(DVQLS_E_ARG);
+    }
+    char* base = static_cast<char*>(opts->workspace_dev);
+    for (auto& r : req) {
+      *r.first = base;
+      ctx->carved.push_back(r.first);
+      base += (r.second + 255) & ~size_t(255);
+    }
+  } else {
+    for (auto& r : req)
+      if (cudaMalloc(r.first, r.second) != cudaSuccess) {
+        fail(ctx, DVQLS_E_CUDA, "cudaMalloc failed");
+        return bail(DVQLS_E_CUDA);
+      }
   }
   ctx->h_stage_bytes = sizeof(double) * std::max<size_t>(size_t(KB) * (ctx->P + 5), 64);
   if (cudaMallocHost((void**)&ctx->h_stage, ctx->h_stage_bytes) != cudaSuccess) {
@@ -883,6 +918,43 @@ int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, 
   }
   *out = ctx;
   return DVQLS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int dvqls_create(dvqls_ctx** out, int n, int layers, int L, const char* paulis, const double* coeffs,
+                 const dvqls_bprep* bprep, const dvqls_opts* opts) {
+  return create_impl(out, n, layers, L, paulis, coeffs, bprep, opts, nullptr);
+}
+
+size_t dvqls_workspace_size(int n, int layers, int L, const dvqls_opts* opts) {
+  if (n < 1 || n > 24 || layers < 1 || L < 1 || double(L) > std::pow(4.0, n)) return 0;
+  // L distinct placeholder strings (base-4 digits of l); only sizes are planned
+  std::string ps(size_t(L) * n, 'I');
+  for (int l = 0; l < L; ++l) {
+    int64_t v = l;
+    for (int q = n - 1; q >= 0 && v; --q, v >>= 2) ps[size_t(l) * n + q] = "IXYZ"[v & 3];
+  }
+  std::vector<double> co(2 * size_t(L), 0.0);
+  co[0] = 1.0;
+  size_t best = 0;
+  const int mode = opts ? opts->mode : DVQLS_MODE_CIRCUITS;
+  for (int kind : {DVQLS_B_UNIFORM, DVQLS_B_AMPLITUDES}) {  // the size for either U_b
+    if (kind == DVQLS_B_AMPLITUDES && (n > 12 || mode != DVQLS_MODE_CIRCUITS)) continue;
+    std::vector<double> amps;
+    dvqls_bprep bp{kind, nullptr};
+    if (kind == DVQLS_B_AMPLITUDES) {
+      amps.assign(2 * (size_t(1) << n), 0.0);
+      amps[0] = 1.0;
+      bp.amps = amps.data();
+    }
+    size_t b = 0;
+    dvqls_ctx* dummy = nullptr;
+    if (create_impl(&dummy, n, layers, L, ps.data(), co.data(), &bp, opts, &b) != DVQLS_OK) return 0;
+    best = std::max(best, b);
+  }
+  return best;
 }
 
 void dvqls_destroy(dvqls_ctx* ctx) {

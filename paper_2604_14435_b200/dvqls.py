@@ -35,7 +35,7 @@ EXPORTED = [
     "dvqls_nccl_unique_id", "dvqls_build_info", "dvqls_shard_range", "dvqls_state",
     "dvqls_terms_subset", "dvqls_launch_grid", "dvqls_num_observables", "dvqls_task_observable",
     "dvqls_costs_dev", "dvqls_global_cost", "dvqls_decompose", "dvqls_pauli_coefficients",
-    "dvqls_decompose_error",
+    "dvqls_decompose_error", "dvqls_workspace_size",
 ]
 
 
@@ -57,7 +57,7 @@ class _Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
                 ("nccl_unique_id", ctypes.c_void_p), ("entangler", ctypes.c_int),
                 ("cuda_stream", ctypes.c_void_p), ("timing", ctypes.c_int), ("max_batch", ctypes.c_int),
-                ("mode", ctypes.c_int)]
+                ("mode", ctypes.c_int), ("workspace_dev", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
 
 
 _lib = None
@@ -105,13 +105,16 @@ def load():
     L.dvqls_task_observable.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, u32p, u32p,
                                         ctypes.POINTER(ctypes.c_int)]
     L.dvqls_last_timings.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
+    L.dvqls_workspace_size.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, vp]
+    L.dvqls_workspace_size.restype = ctypes.c_size_t
     L.dvqls_nccl_unique_id.argtypes = [vp]
     L.dvqls_build_info.restype = ctypes.c_char_p
     L.dvqls_shard_range.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
                                     ctypes.POINTER(ctypes.c_int64)]
     for name in EXPORTED:
         if name not in ("dvqls_destroy", "dvqls_last_error", "dvqls_num_circuits", "dvqls_stream",
-                        "dvqls_build_info", "dvqls_num_observables", "dvqls_decompose_error"):
+                        "dvqls_build_info", "dvqls_num_observables", "dvqls_decompose_error",
+                        "dvqls_workspace_size"):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -155,7 +158,10 @@ class Context:
 
     def __init__(self, n, layers, paulis: bytes, coeffs, bkind=DVQLS_B_UNIFORM, b=None, device=-1, rank=0,
                  world=1, nccl_id: bytes | None = None, entangler=0, stream=None, timing=False, max_batch=16,
-                 mode=0):
+                 mode=0, workspace=None):
+        """workspace: None (the library allocates its device tables once, here) or caller-owned device
+        memory -- a CUDA torch tensor (kept alive by the context) or an (address, bytes) pair -- of at
+        least workspace_size(...) bytes, 256-byte aligned (dvqls_opts.workspace_dev)."""
         L = load()
         self.n, self.layers = int(n), int(layers)
         self.P = 3 * self.n * self.layers
@@ -178,8 +184,15 @@ class Context:
         sp = None
         if stream is not None:
             sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        wp, wb = None, 0
+        if workspace is not None:
+            if hasattr(workspace, "data_ptr"):
+                wp, wb = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+                self._keep.append(workspace)
+            else:
+                wp, wb = int(workspace[0]), int(workspace[1])
         op = _Opts(device, rank, world, ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None,
-                   entangler, sp, 1 if timing else 0, max_batch, mode)
+                   entangler, sp, 1 if timing else 0, max_batch, mode, wp, wb)
         h = ctypes.c_void_p()
         rc = L.dvqls_create(ctypes.byref(h), self.n, self.layers, self.L, paulis, _dp(co), ctypes.byref(bp),
                             ctypes.byref(op))
@@ -290,6 +303,12 @@ class Context:
 
 
 # C-ABI-named functional wrappers --------------------------------------------------
+def workspace_size(n_qubits, layers, n_terms, device=-1, rank=0, world=1, max_batch=16, mode=0) -> int:
+    """dvqls_workspace_size: device bytes a context carves from a caller workspace (0 = invalid)."""
+    op = _Opts(device, rank, world, None, 0, None, 0, max_batch, mode, None, 0)
+    return int(load().dvqls_workspace_size(int(n_qubits), int(layers), int(n_terms), ctypes.byref(op)))
+
+
 def dvqls_create(n_qubits, layers, pauli_terms: bytes, coeffs, b_prep=(DVQLS_B_UNIFORM, None), **opts) -> Context:
     kind, amps = b_prep
     return Context(n_qubits, layers, pauli_terms, coeffs, kind, amps, **opts)

@@ -156,3 +156,28 @@ def test_device_resident_entry_point(dv):
         assert abs(out[0].item() - ctx_c) < 1e-14
     finally:
         ctx.destroy()
+
+
+@pytest.mark.parametrize("n,amp", [(4, True), (10, False), (13, False)])
+def test_torch_workspace(dv, n, amp):
+    """dvqls_workspace_size + opts.workspace_dev: a context carving its device tables from a torch
+    tensor gives bitwise the same terms and cost as one that allocates them itself; a workspace
+    too small for the context (the size covers either U_b, so "too small" is checked with 4 KB)
+    is rejected with DVQLS_E_ARG."""
+    import torch
+    w = configs.random_workload(n, 3, 2, seed=300 + n, amplitudes=amp)
+    th = w.theta0()
+    need = dv.workspace_size(w.n, w.layers, w.L, max_batch=4)
+    assert need > 0
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    a = dv.from_workload(w, max_batch=4, workspace=ws)
+    b = dv.from_workload(w, max_batch=4)
+    try:
+        assert np.array_equal(a.terms(th), b.terms(th))
+        assert a.cost(th) == b.cost(th)
+    finally:
+        a.destroy()
+        b.destroy()
+    with pytest.raises(dv.DvqlsError) as ei:
+        dv.from_workload(w, max_batch=4, workspace=(ws.data_ptr(), 4096))
+    assert ei.value.code == dv.DVQLS_E_ARG
