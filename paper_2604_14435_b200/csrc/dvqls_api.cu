@@ -140,7 +140,8 @@ struct dvqls_ctx {
   ncclComm_t comm = nullptr;
 
   KernelCfg kc;
-  int grid = 0;     // CTAs per theta
+  int grid = 0;     // CTAs per theta (tile path) / for one theta (register path)
+  int grid_cap = 0; // register path: resident CTAs (SMs x occupancy), the cap of a K-theta launch
   int64_t NG = 0;   // circuit groups per theta
   int prefix_threads = 0;
   int prefix_rb = 3;
@@ -295,6 +296,10 @@ int launch_hadamard(dvqls_ctx* ctx, int K, int64_t c0, int64_t C, const int64_t*
   if (ctx->tile_path && ctx->n > ctx->tile_bits) grid = std::max(1, grid / K);  // scratch: grid CTAs in total
   dim3 g(grid, K);
   if (!ctx->tile_path) {  // one persistent 1-D grid over the flattened K x C work (kernels.cuh)
+    // enough CTAs for all K thetas' circuits, up to one resident wave (a grid sized for one
+    // theta would leave most SMs idle on small problems evaluated in large batches)
+    grid = int(std::max<int64_t>(
+        1, std::min<int64_t>(ctx->grid_cap, (int64_t(K) * C + ctx->kc.groups - 1) / std::max(1, ctx->kc.groups))));
     void* args[] = {(void*)&ctx->d_x,   (void*)&ctx->d_tab, (void*)&ctx->d_coef,  (void*)&ctx->d_hv,
                     (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&c0, (void*)&C, (void*)&K,
                     (void*)&terms, (void*)&ctx->d_partials, (void*)&with_cost, (void*)&red_out,
@@ -664,7 +669,8 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
   }
   const int64_t need = (Cloc + groups_per_cta - 1) / groups_per_cta;
   ctx->grid = int(std::max<int64_t>(1, std::min(want, need)));
-  ctx->NG = int64_t(ctx->grid) * groups_per_cta;
+  ctx->grid_cap = int(std::max<int64_t>(1, want));
+  ctx->NG = std::max<int64_t>(int64_t(ctx->grid) * groups_per_cta, ctx->tile_path ? 0 : ctx->grid_cap);
   // Team mode is opt-in (DVQLS_TEAM=1): measured on B200 it cuts DRAM reads ~10x but the team
   // barriers cost as much as they save (cfg5 n=16: 210 vs 217 ms, n=18: 1218 vs 1123 ms, K=2).
   if (ctx->tile_path && n >= 15 && ctx->mode == DVQLS_MODE_CIRCUITS && getenv("DVQLS_TEAM") &&
