@@ -82,6 +82,16 @@ def test_no_gpu_fails_loudly(lib):
         dvqls.Context(2, 1, b"IXZY", np.ones(4))
 
 
+def test_workspace_size_arguments(lib):
+    """dvqls_workspace_size returns 0 for invalid shapes (n, layers, L out of range, more terms
+    than Pauli strings) and, without a usable sm_100 device, 0 instead of a guess."""
+    for args in ((0, 1, 1), (25, 1, 1), (4, 0, 1), (4, 1, 0), (1, 1, 5)):
+        assert dvqls.workspace_size(*args) == 0
+    import torch
+    if not torch.cuda.is_available():
+        assert dvqls.workspace_size(10, 10, 64) == 0
+
+
 def test_shard_ranges_tile_the_circuits(lib):
     for C in (0, 1, 7, 2560, 90112, 360448):
         for W in (1, 2, 3, 4, 8):
