@@ -188,23 +188,25 @@ def streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, grid=None):
 
 
 def onchip_roofline(w, local_c, KT, had_ms, sms, fmax, peak_src):
-    """n = 11, 12 (stream.cuh single tile): FP64-pipe ops vs 64 lanes/clk/SM; on-chip bytes =
-    4 SMEM exchanges per numerator circuit (STS + LDS of the 16N-byte branch each: 128N) plus x
-    gathered twice from L1/L2 (32N, not SMEM)."""
+    """n = 11, 12 (one tile on chip): FP64-pipe ops vs 64 lanes/clk/SM; on-chip bytes = the SURVEY
+    §8(d) model of the register path (96N per numerator circuit: x read twice + one exchange per
+    FWHT; 32N per denominator), which the default 2-exchange kernel (onchip_plane.cuh) implements
+    (its x reads come from L2 through the L1 pipe).  With DVQLS_ONCHIP=0 the 4-exchange tile
+    kernel runs against the same model."""
     ops = fp64_ops_per_eval(w, local_c) * KT
-    N = 1 << w.n
-    s = (local_c // 2) % (w.n + 1)
-    num = int(np.count_nonzero(s))
-    sbytes = num * 128 * N * KT
+    sbytes = smem_bytes_per_eval(w, local_c) * KT
     fp64_peak = 64 * sms * fmax
     smem_peak = 128 * sms * fmax
     t = had_ms * 1e-3
-    return {"bound": "alu", "kernel": f"stream_hadamard_kernel<{11 if w.n == 11 else 12}>",
+    onchip = w.bkind == 0 and os.environ.get("DVQLS_ONCHIP", "1") != "0" and os.environ.get("DVQLS_PLANE", "1") != "0"
+    kern = (f"onchip_plane_kernel<{w.n}>" if onchip else
+            f"stream_{'plane' if w.bkind == 0 and os.environ.get('DVQLS_PLANE', '1') != '0' else 'hadamard'}_kernel<{11 if w.n == 11 else 12}>")
+    return {"bound": "alu", "kernel": kern,
             "achieved": ops / t / 1e12, "peak": fp64_peak / 1e12, "unit": "Top/s", "frac": ops / t / fp64_peak,
             "traffic": None,
             "smem": {"achieved": sbytes / t / 1e9, "peak": smem_peak / 1e9, "unit": "GB/s",
                      "frac": sbytes / t / smem_peak,
-                     "note": "4 exchanges (STS + LDS) of the branch per numerator circuit = 128N bytes"},
+                     "note": "on-chip model bytes: 96N per numerator circuit, 32N per denominator"},
             "model_frac": max(ops / fp64_peak, sbytes / smem_peak) / t,
             "note": (f"FP64-pipe lane-ops per launch = {ops:.4g} / mean CUDA-event kernel time; peak = 64 "
                      f"lanes/clk/SM x {sms} SMs x sm_max_mhz ({peak_src} MEASURED_PEAKS.json)")}

@@ -26,6 +26,7 @@
 #include "tile.cuh"
 #include "stream.cuh"
 #include "stream_plane.cuh"
+#include "onchip_plane.cuh"
 #include "pauli.cuh"
 #include "global.cuh"
 #include "decomp.cuh"
@@ -174,6 +175,8 @@ struct dvqls_ctx {
   int tile_bits = 12;            // tile path: amplitudes per SMEM tile = 2^tile_bits
   double2* d_scratch = nullptr;  // grid * N (n > 12; doubles when pstream)
   bool pstream = false;          // n >= 11, uniform b: real-plane streaming kernel (stream_plane.cuh)
+  bool onchip = false;           // n = 11, 12, uniform b: 2-exchange real-plane kernel (onchip_plane.cuh)
+  double* d_xq = nullptr;        // onchip: [K][x_re | -x_re | x_im | -x_im]
   double* d_xp = nullptr;        // planar copy of x for pstream: [K][re N | im N]
   std::vector<void**> carved;    // device buffers carved from a caller workspace (not freed)
   double2* d_x2 = nullptr;       // ring ping-pong buffer (n > 12 prefix)
@@ -305,6 +308,17 @@ int launch_hadamard(dvqls_ctx* ctx, int K, int64_t c0, int64_t C, const int64_t*
                     (void*)&terms, (void*)&ctx->d_partials, (void*)&with_cost, (void*)&red_out,
                     (void*)&ctx->d_counter, (void*)&p2p};
     CK(cudaLaunchKernel(ctx->kc.fn, dim3(grid), dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
+  } else if (ctx->onchip) {  // [x_re | -x_re | x_im | -x_im], then the 2-exchange kernel, 1-D grid
+    const size_t blk = sizeof(double) * 4 * size_t(ctx->N);  // one theta's x block, a power of two
+    double* xq = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ctx->d_xq) + blk - 1) & ~uintptr_t(blk - 1));
+    onchip::to_planar4_kernel<<<std::min<int64_t>(1184, (int64_t(K) * ctx->N + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->d_x, uint32_t(ctx->N), uint32_t(K), xq);
+    const int g1 = int(std::max<int64_t>(
+        1, std::min<int64_t>(ctx->grid_cap, (int64_t(K) * C + ctx->kc.groups - 1) / std::max(1, ctx->kc.groups))));
+    void* args[] = {(void*)&xq, (void*)&ctx->d_tab, (void*)&ctx->d_coef, (void*)&ctx->L, (void*)&c0,
+                    (void*)&C, (void*)&K, (void*)&terms, (void*)&ctx->d_partials, (void*)&with_cost,
+                    (void*)&red_out, (void*)&ctx->d_counter, (void*)&p2p};
+    CK(cudaLaunchKernel(ctx->kc.fn, dim3(g1), dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
   } else if (ctx->pstream) {  // planar x, then the real-plane streaming kernel
     streamp::to_planar_kernel<<<std::min<int64_t>(1184, (int64_t(K) * ctx->N + 255) / 256), 256, 0, ctx->stream>>>(
         ctx->d_x, uint32_t(ctx->N), uint32_t(K), ctx->d_xp);
@@ -409,7 +423,7 @@ void release(dvqls_ctx* c) {
   cudaFree(c->d_obs); cudaFree(c->d_wE); cudaFree(c->d_wP); cudaFree(c->d_task); cudaFree(c->d_e);
   cudaFree(c->d_team_acc); cudaFree(c->d_team_ctr);
   cudaFree(c->d_b); cudaFree(c->d_beta); cudaFree(c->d_out6); cudaFree(c->d_gcounter);
-  cudaFree(c->d_counter); cudaFree(c->d_scratch); cudaFree(c->d_xp); cudaFree(c->d_x2); cudaFree(c->d_gates); cudaFree(c->d_cidx); cudaFree(c->d_sub);
+  cudaFree(c->d_counter); cudaFree(c->d_scratch); cudaFree(c->d_xp); cudaFree(c->d_xq); cudaFree(c->d_x2); cudaFree(c->d_gates); cudaFree(c->d_cidx); cudaFree(c->d_sub);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -639,6 +653,18 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
       ctx->kc.fn = ctx->tile_bits == 11 ? (const void*)&streamp::stream_plane_kernel<11>
                                         : (const void*)&streamp::stream_plane_kernel<12>;
       ctx->kc.smem = ctx->tile_bits == 11 ? streamp::tile_smem<11>() : streamp::tile_smem<12>();
+      // n = 11, 12 (one tile): the 2-exchange kernel with 64 doubles per thread (DVQLS_ONCHIP=0:
+      // keep the 4-exchange tile kernel, A/B knob)
+      const char* oe = getenv("DVQLS_ONCHIP");
+      if (n <= 12 && !(oe && atoi(oe) == 0)) {
+        ctx->pstream = false;
+        ctx->onchip = true;
+        ctx->kc.fn = n == 11 ? (const void*)&onchip::onchip_plane_kernel<11>
+                             : (const void*)&onchip::onchip_plane_kernel<12>;
+        ctx->kc.warps = onchip::WARPS;
+        ctx->kc.groups = n == 11 ? onchip::Sh<11>::NG : onchip::Sh<12>::NG;
+        ctx->kc.smem = n == 11 ? onchip::smem_bytes<11>() : onchip::smem_bytes<12>();
+      }
     }
   }
   if (cudaFuncSetAttribute(ctx->kc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->kc.smem)) !=
@@ -657,7 +683,8 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
   dvqls_shard_range(ctx->C, ctx->rank, ctx->world, &ctx->c0, &ctx->c1);
   ctx->chunk = (ctx->C + ctx->world - 1) / ctx->world;
   const int64_t Cloc = ctx->c1 - ctx->c0;
-  const int64_t groups_per_cta = ctx->tile_path ? 1 : int64_t(ctx->kc.groups);
+  const bool flat_grid = !ctx->tile_path || ctx->onchip;  // one 1-D grid over the K x C work
+  const int64_t groups_per_cta = flat_grid ? int64_t(ctx->kc.groups) : 1;
   int64_t want = int64_t(prop.multiProcessorCount) * occ;
   if (ctx->tile_path && n > ctx->tile_bits) {  // each CTA owns a 2^n-amplitude global scratch
     const int64_t cap = int64_t(kScratchBudget / ((ctx->pstream ? sizeof(double) : sizeof(double2)) * size_t(ctx->N)));
@@ -670,7 +697,7 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
   const int64_t need = (Cloc + groups_per_cta - 1) / groups_per_cta;
   ctx->grid = int(std::max<int64_t>(1, std::min(want, need)));
   ctx->grid_cap = int(std::max<int64_t>(1, want));
-  ctx->NG = std::max<int64_t>(int64_t(ctx->grid) * groups_per_cta, ctx->tile_path ? 0 : ctx->grid_cap);
+  ctx->NG = std::max<int64_t>(int64_t(ctx->grid) * groups_per_cta, flat_grid ? ctx->grid_cap : 0);
   // Team mode is opt-in (DVQLS_TEAM=1): measured on B200 it cuts DRAM reads ~10x but the team
   // barriers cost as much as they save (cfg5 n=16: 210 vs 217 ms, n=18: 1218 vs 1123 ms, K=2).
   if (ctx->tile_path && n >= 15 && ctx->mode == DVQLS_MODE_CIRCUITS && getenv("DVQLS_TEAM") &&
@@ -836,6 +863,8 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
   buffer(n > 12 && ctx->mode == DVQLS_MODE_CIRCUITS, &ctx->d_scratch,
        (ctx->pstream ? sizeof(double) : sizeof(double2)) * size_t(ctx->team ? ctx->nteams : ctx->grid) * ctx->N);
   buffer(ctx->pstream, &ctx->d_xp, sizeof(double2) * KB * ctx->N);
+  // onchip: every theta's 4N-double x block aligned to its size (XOR addressing); slack for the round-up
+  buffer(ctx->onchip, &ctx->d_xq, sizeof(double) * 4 * (size_t(KB) + 1) * ctx->N);
   buffer(ctx->team, &ctx->d_team_acc, sizeof(double) * 2 * size_t(ctx->nteams) * ctx->team);
   buffer(ctx->team, &ctx->d_team_ctr, sizeof(unsigned) * (size_t(ctx->nteams) + 1));
   const bool pm = ctx->mode == DVQLS_MODE_PAULI;
@@ -1098,7 +1127,7 @@ int dvqls_terms_subset(dvqls_ctx* ctx, const double* theta, const int64_t* idx, 
   for (int64_t i = 0; i < count; ++i)
     if (idx[i] < 0 || idx[i] >= ctx->C) return fail(ctx, DVQLS_E_ARG, "circuit index %lld out of range", (long long)idx[i]);
   if (count == 0) return DVQLS_OK;
-  if (!ctx->tile_path || ctx->world > 1 || ctx->mode == DVQLS_MODE_PAULI) {  // evaluate all, pick entries
+  if (!ctx->tile_path || ctx->onchip || ctx->world > 1 || ctx->mode == DVQLS_MODE_PAULI) {  // all, pick
     std::vector<double> all(size_t(ctx->C));
     int rc = dvqls_terms(ctx, theta, all.data());
     if (rc) return rc;
@@ -1350,7 +1379,7 @@ int dvqls_launches_per_call(const dvqls_ctx* ctx) {
   // prefix (1, or 2 + layers*(groups+1) for the global n > 12 prefix), hadamard (+ fused
   // reduction) [, finalize]  (+ NCCL's own allreduce kernel when world > 1)
   const int pre = ctx->prefix_rb < 0 ? 2 + ctx->layers * ((ctx->n <= 21 ? 2 : 3) + 1) : 1;
-  return pre + 1 + (ctx->pstream ? 1 : 0) + ((ctx->world == 1 || ctx->p2p) ? 0 : 1);
+  return pre + 1 + ((ctx->pstream || ctx->onchip) ? 1 : 0) + ((ctx->world == 1 || ctx->p2p) ? 0 : 1);
 }
 
 int dvqls_last_timings(const dvqls_ctx* c, float* ms) {
