@@ -549,7 +549,8 @@ def main():
                 "workload": w.name, "n_qubits": w.n, "L": w.L, "layers": w.layers,
                 "circuits_per_eval": w.n_circuits, "thetas_per_step": KT,
                 "l2": "flushed before every step (256 MiB write, outside the timed events)",
-                "parallelism": f"dp{world} (contiguous circuit blocks, one NCCL allreduce of 4 fp64 per theta)",
+                "parallelism": (f"dp{world} (contiguous circuit blocks; 4 fp64 per theta summed across ranks by the "
+                                "Hadamard kernel's tail over NVLink peer memory, NCCL allreduce as the fallback)"),
             },
             "evals_per_s": KT * args.steps / (dev_ms * 1e-3),
             "k1": {"value": w.n_circuits * k1_steps / (k1_ms * 1e-3), "unit": "circuits/s",
