@@ -172,7 +172,9 @@ def streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, grid=None):
     b96 = smem_bytes_per_eval(w, local_c) * KT
     ach = b / (had_ms * 1e-3)
     peak = float(peaks["hbm_gbs"]) * 1e9
-    out = {"bound": "hbm", "kernel": "stream_hadamard_kernel<12>", "achieved": ach / 1e9, "peak": peak / 1e9,
+    plane = w.bkind == 0 and os.environ.get("DVQLS_PLANE", "1") != "0" and os.environ.get("DVQLS_TEAM", "0") != "1"
+    kern = "stream_plane_kernel<12>" if plane else "stream_hadamard_kernel<12>"
+    out = {"bound": "hbm", "kernel": kern, "achieved": ach / 1e9, "peak": peak / 1e9,
            "unit": "GB/s", "frac": ach / peak, "traffic": None,
            "model96_GBps": b96 / (had_ms * 1e-3) / 1e9,
            "note": (f"algorithmic DRAM bytes per launch = {b:.4g} (64N per numerator circuit: 3 passes "
@@ -180,7 +182,7 @@ def streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, grid=None):
                     f"CUDA-event kernel time; peak = hbm_gbs of {peak_src} MEASURED_PEAKS.json. model96_GBps "
                     f"= the SURVEY §8(d) 96N model (x reads counted as HBM)")}
     if grid is not None:
-        scratch = grid * (1 << w.n) * 16
+        scratch = grid * (1 << w.n) * (8 if plane else 16)
         out["scratch_bytes"] = scratch
         if scratch <= 100 << 20:
             out["note"] += "; the per-CTA scratch fits in L2 at this n, so L2 bandwidth, not HBM, bounds it"
