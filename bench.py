@@ -292,6 +292,8 @@ def main():
                          "config-2 L-BFGS-B loop calls the path; K=1 is measured and reported beside it")
     ap.add_argument("--n", type=int, default=16, help="qubits for --config cfg5 (12..24)")
     ap.add_argument("--impl", default="dvqls", choices=["dvqls", "reference"])
+    ap.add_argument("--slice", type=int, default=0,
+                    help="weak-scaling reference (1 GPU only): evaluate rank 0's block of a SLICE-way split")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-next2", action="store_true", help="skip the NEXT-2 fast-path side measurement")
     args = ap.parse_args()
@@ -327,6 +329,10 @@ def main():
     KT = args.batch
     chars, co = w.arrays()
     # device memory comes from torch: the library carves its tables from this workspace
+    if args.slice > 1:
+        if world > 1:
+            raise SystemExit("--slice is the 1-GPU weak-scaling reference")
+        os.environ["DVQLS_SLICE"] = f"0/{args.slice}"
     ws_bytes = dvqls.workspace_size(w.n, w.layers, w.L, device=local, rank=rank, world=world,
                                     max_batch=max(KT, 1))
     workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
@@ -515,7 +521,8 @@ def main():
         pctx.destroy()
 
     # ---- derived numbers -------------------------------------------------------------------------
-    circuits_step = w.n_circuits * KT
+    n_eval = (c1 - c0) if args.slice > 1 else w.n_circuits  # circuits this job evaluates per theta
+    circuits_step = n_eval * KT
     value = circuits_step * args.steps / (dev_ms * 1e-3)
     e2e_value = circuits_step * args.steps / e2e_s
     had_ms = statistics.mean(t["hadamard_ms"] for t in kt)
@@ -553,9 +560,11 @@ def main():
                 "l2": "flushed before every step (256 MiB write, outside the timed events)",
                 "parallelism": (f"dp{world} (contiguous circuit blocks; 4 fp64 per theta summed across ranks by the "
                                 "Hadamard kernel's tail over NVLink peer memory, NCCL allreduce as the fallback)"),
+                **({"slice": f"rank 0's block of a {args.slice}-way split ({n_eval} circuits per theta): the "
+                             "1-GPU weak-scaling reference"} if args.slice > 1 else {}),
             },
             "evals_per_s": KT * args.steps / (dev_ms * 1e-3),
-            "k1": {"value": w.n_circuits * k1_steps / (k1_ms * 1e-3), "unit": "circuits/s",
+            "k1": {"value": n_eval * k1_steps / (k1_ms * 1e-3), "unit": "circuits/s",
                    "ms_per_step": k1_ms / k1_steps, "evals_per_s": k1_steps / (k1_ms * 1e-3),
                    "kernel_ms": {"prefix": statistics.mean(t["prefix_ms"] for t in k1t),
                                  "hadamard": statistics.mean(t["hadamard_ms"] for t in k1t),

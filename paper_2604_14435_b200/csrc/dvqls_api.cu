@@ -681,6 +681,13 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
 
   ctx->C = 2 * int64_t(n + 1) * L * L;
   dvqls_shard_range(ctx->C, ctx->rank, ctx->world, &ctx->c0, &ctx->c1);
+  if (ctx->world == 1 && getenv("DVQLS_SLICE")) {
+    // measurement knob (weak-scaling reference, SURVEY §8(d) cfg 4): evaluate only rank r's block
+    // of a W-way split on this one GPU ("r/W"); costs then cover that block only
+    int r = 0, W = 1;
+    if (sscanf(getenv("DVQLS_SLICE"), "%d/%d", &r, &W) == 2 && W >= 1 && r >= 0 && r < W)
+      dvqls_shard_range(ctx->C, r, W, &ctx->c0, &ctx->c1);
+  }
   ctx->chunk = (ctx->C + ctx->world - 1) / ctx->world;
   const int64_t Cloc = ctx->c1 - ctx->c0;
   const bool flat_grid = !ctx->tile_path || ctx->onchip;  // one 1-D grid over the K x C work
