@@ -250,13 +250,15 @@ def run_reference(args, w):
     from oracle import sim
     cores = sim.hardware_threads()
     theta = w.theta0()
-    # size one step to ~3 s of faithful-mode work on all cores
+    # size one step to ~3 s of faithful-mode work on all cores, less when many steps are asked for,
+    # so the whole --steps K run stays within ~2 minutes
+    step_s = min(3.0, 120.0 / max(args.steps, 1))
     n_probe = max(cores, 8)
     idx = np.linspace(0, w.n_circuits - 1, n_probe).astype(np.int64)
     t0 = time.perf_counter()
     sim.workload_terms(w, theta, mode=0, idx=idx, nthreads=cores)
     per = (time.perf_counter() - t0) / n_probe
-    m = int(min(w.n_circuits, max(n_probe, 3.0 / max(per, 1e-9))))
+    m = int(min(w.n_circuits, max(n_probe, step_s / max(per, 1e-9))))
     idx = np.linspace(0, w.n_circuits - 1, m).astype(np.int64)
     for _ in range(args.warmup):
         sim.workload_terms(w, theta, mode=0, idx=idx[: max(1, m // 10)], nthreads=cores)
