@@ -12,6 +12,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdarg>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -689,6 +690,11 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
       dvqls_shard_range(ctx->C, r, W, &ctx->c0, &ctx->c1);
   }
   ctx->chunk = (ctx->C + ctx->world - 1) / ctx->world;
+  if (ctx->c1 - ctx->c0 > int64_t(INT32_MAX)) {  // the kernels index a rank's circuits with 32-bit ints
+    fail(ctx, DVQLS_E_UNSUPPORTED, "%lld circuits on one rank (more than 2^31 - 1): use more ranks",
+         (long long)(ctx->c1 - ctx->c0));
+    return bail(DVQLS_E_UNSUPPORTED);
+  }
   const int64_t Cloc = ctx->c1 - ctx->c0;
   const bool flat_grid = !ctx->tile_path || ctx->onchip;  // one 1-D grid over the K x C work
   const int64_t groups_per_cta = flat_grid ? int64_t(ctx->kc.groups) : 1;

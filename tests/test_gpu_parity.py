@@ -181,3 +181,14 @@ def test_torch_workspace(dv, n, amp):
     with pytest.raises(dv.DvqlsError) as ei:
         dv.from_workload(w, max_batch=4, workspace=(ws.data_ptr(), 4096))
     assert ei.value.code == dv.DVQLS_E_ARG
+
+
+def test_too_many_circuits_per_rank_is_rejected(dv):
+    """2(n+1)L^2 > 2^31 - 1 circuits on one rank (n = 10, L = 10,000) is DVQLS_E_UNSUPPORTED, not
+    a silent 32-bit overflow in the kernels' circuit indices."""
+    n, L = 10, 10000
+    s = np.base_repr  # distinct strings: base-4 digits of l over IXYZ
+    terms = b"".join(s(l, 4).rjust(n, "0").translate(str.maketrans("0123", "IXYZ")).encode() for l in range(L))
+    with pytest.raises(dv.DvqlsError) as ei:
+        dv.Context(n, 1, terms, np.ones(2 * L))
+    assert ei.value.code == dv.DVQLS_E_UNSUPPORTED

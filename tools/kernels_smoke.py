@@ -1,6 +1,6 @@
 """Small runs of every kernel family (compute-sanitizer is closed on the GPU pool; this is the plain check):
 n = 4 (complex register kernel, Householder b), n = 10 (real-plane kernel, K = 3 batch),
-n = 12 (single-tile real-plane streaming kernel), n = 13 (multi-pass streaming), Pauli mode,
+n = 12 (two-exchange on-chip kernel), n = 13 (multi-pass real-plane streaming), Pauli mode,
 global cost, and the NEXT-4 decomposition at n = 9.  Each result is checked against the oracle
 so a sanitizer-clean run is also a correct one."""
 import os
