@@ -56,19 +56,20 @@ def fp64_ops_per_eval(w, circuits=None):
 
 
 def hbm_bytes_per_eval(w, circuits=None):
-    """Streaming-path algorithmic DRAM bytes (n > 12, stream.cuh): the branch of a numerator
-    circuit makes 3 passes through its per-CTA scratch (P0 writes 16N, P1 reads + writes 32N,
-    P2 reads 16N: 64N) while x (<= 64 MB for n <= 22) stays L2-resident; n >= 23 takes 5 passes
-    (128N) and x (128-256 MB) is read from DRAM twice (32N, also by the denominators).
-    SURVEY §8(d) counts x as HBM traffic too (96N); that figure is reported beside it."""
+    """Streaming-path algorithmic DRAM bytes (n > 12): the branch of a numerator circuit makes 3
+    passes through its per-CTA scratch (P0 writes 16N, P1 reads + writes 32N, P2 reads 16N: 64N)
+    while x (K x <= 32 MB for n <= 21) stays L2-resident; from n = 22 x (K x 64-256 MB) is read from
+    DRAM twice (32N, also by the denominators), and n >= 23 takes 5 passes (128N).
+    SURVEY §8(d) counts x as HBM traffic at every n (96N); that figure is reported beside it."""
     N = 1 << w.n
     c = np.arange(w.n_circuits) if circuits is None else circuits
     s = (c // 2) % (w.n + 1)
     num = int(np.count_nonzero(s))
     den = c.size - num
-    if w.n <= 22:
+    if w.n <= 21:
         return num * 64 * N
-    return num * 160 * N + den * 32 * N
+    passes = 64 if w.n <= 22 else 128
+    return num * (passes + 32) * N + den * 32 * N
 
 
 def smem_bytes_per_eval(w, circuits=None):
