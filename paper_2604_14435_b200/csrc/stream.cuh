@@ -461,7 +461,7 @@ stream_hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __res
   const int64_t cb = (int64_t)blockIdx.x * C / G, ce = ((int64_t)blockIdx.x + 1) * C / G;
   const uint32_t ntiles = N > uint32_t(T::TN) ? N >> TB : 1u;
   const Geo g0 = group(n, 0, TB);
-  const bool big_x = n >= 22;  // x (K x 64 MB at n = 22) no longer L2-resident: prefetch its tiles too
+  const bool big_x = n > 22;  // x tiles prefetched too (measured at n = 22: no gain, x of 2 thetas ~ L2)
   if (t == 0) acc4[0] = acc4[1] = acc4[2] = acc4[3] = 0.0;
 
   for (int64_t cl = cb; cl < ce; ++cl) {
@@ -619,7 +619,7 @@ stream_team_kernel(const double2* __restrict__ x_all, const PauliTerm* __restric
   const uint32_t ntiles = N >> TB;
   const uint32_t ta = uint32_t(uint64_t(r) * ntiles / T), tb = uint32_t(uint64_t(r + 1) * ntiles / T);
   const Geo g0 = group(n, 0, TB);
-  const bool big_x = n >= 22;  // x no longer L2-resident (K x 64 MB at n = 22): prefetch its tiles too
+  const bool big_x = n > 22;  // x tiles prefetched too (measured at n = 22: no gain, x of 2 thetas ~ L2)
   double2* __restrict__ phi = scratch + size_t(g) * N;
   unsigned* ctr = team_ctr + g;
   unsigned bars = 0;

@@ -314,7 +314,7 @@ stream_plane_kernel(const double* __restrict__ x_all, const PauliTerm* __restric
   const int64_t cb = (int64_t)blockIdx.x * C / G, ce = ((int64_t)blockIdx.x + 1) * C / G;
   const uint32_t ntiles = N > uint32_t(T::TN) ? N >> TB : 1u;
   const Geo g0 = stream::group(n, 0, TB);
-  const bool big_x = n >= 22;  // x no longer L2-resident (K x 64 MB at n = 22): prefetch its tiles too
+  const bool big_x = n > 22;  // x tiles prefetched too (measured at n = 22: no gain, x of 2 thetas ~ L2)
   if (t == 0) acc4[0] = acc4[1] = acc4[2] = acc4[3] = 0.0;
 
   for (int64_t cl = cb; cl < ce; ++cl) {
