@@ -174,7 +174,9 @@ def streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, grid=None):
     ach = b / (had_ms * 1e-3)
     peak = float(peaks["hbm_gbs"]) * 1e9
     plane = w.bkind == 0 and os.environ.get("DVQLS_PLANE", "1") != "0" and os.environ.get("DVQLS_TEAM", "0") != "1"
-    kern = "stream_plane_kernel<12>" if plane else "stream_hadamard_kernel<12>"
+    staged = os.environ.get("DVQLS_STAGE", "") != "0" and (w.n >= 16 or os.environ.get("DVQLS_STAGE") == "1")
+    kern = (f"stream_plane_kernel<12, {'TMA-staged' if staged else 'direct'}>" if plane
+            else "stream_hadamard_kernel<12>")
     out = {"bound": "hbm", "kernel": kern, "achieved": ach / 1e9, "peak": peak / 1e9,
            "unit": "GB/s", "frac": ach / peak, "traffic": None,
            "model96_GBps": b96 / (had_ms * 1e-3) / 1e9,

@@ -654,6 +654,15 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
       ctx->kc.fn = ctx->tile_bits == 11 ? (const void*)&streamp::stream_plane_kernel<11>
                                         : (const void*)&streamp::stream_plane_kernel<12>;
       ctx->kc.smem = ctx->tile_bits == 11 ? streamp::tile_smem<11>() : streamp::tile_smem<12>();
+      // n >= 16 (scratch no longer L2-resident): TMA bulk-copy staging of the last-pass and
+      // large-run mid-pass tiles (measured +1-3 % at n = 16..20, -5 % at n = 14 where the scratch
+      // stays in L2; DVQLS_STAGE=0 keeps direct register loads + L2 prefetch, =1 forces it from n = 13)
+      const char* se = getenv("DVQLS_STAGE");
+      const int stage_from = se && atoi(se) == 1 ? 13 : 16;
+      if (n >= stage_from && ctx->tile_bits == 12 && !(se && atoi(se) == 0)) {
+        ctx->kc.fn = (const void*)&streamp::stream_plane_kernel<12, true>;
+        ctx->kc.smem = streamp::staged_smem<12>();
+      }
       // n = 11, 12 (one tile): the 2-exchange kernel with 64 doubles per thread (DVQLS_ONCHIP=0:
       // keep the 4-exchange tile kernel, A/B knob)
       const char* oe = getenv("DVQLS_ONCHIP");

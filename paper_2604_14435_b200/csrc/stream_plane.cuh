@@ -18,6 +18,8 @@
 // arithmetic per element).
 #pragma once
 
+#include <type_traits>
+
 #include "stream.cuh"
 
 namespace dvqls {
@@ -53,7 +55,12 @@ __device__ __forceinline__ void sts(uint32_t a, double v) {
 __host__ __device__ constexpr uint32_t pslot(uint32_t e) { return e + (e >> 4); }
 template <int TB>
 __host__ __device__ constexpr size_t tile_smem() {
-  return sizeof(double) * pslot(1u << TB);
+  return (sizeof(double) * pslot(1u << TB) + 15) & ~size_t(15);
+}
+// exchange tile + TMA staging tile + mbarrier (STAGED kernels)
+template <int TB>
+__host__ __device__ constexpr size_t staged_smem() {
+  return tile_smem<TB>() + sizeof(double) * (size_t(1) << TB) + 16;
 }
 
 // &base[idx] (8-byte elements) as one IMAD.WIDE.U32
@@ -156,6 +163,69 @@ __device__ __forceinline__ void gstore(const double (&v)[16], double* __restrict
   }
 }
 
+// ---- TMA bulk-copy staging of tiles (STAGED kernels) -----------------------------------------
+// The tile of the NEXT iteration is copied global -> SMEM by cp.async.bulk (the TMA engine, SASS
+// UBLKCP) into a staging buffer while the current tile is transformed in registers; completion is
+// tracked by an mbarrier (expect_tx by thread 0, complete_tx by the copies).  The staging buffer
+// holds the tile in natural element order, so the register layouts LM and LH read it conflict-free
+// (a half-warp's 16 doubles are consecutive) with base + immediate addressing.
+struct Stager {
+  uint32_t buf;    // shared-window address of 2^TB staged doubles
+  uint32_t mbar;   // shared-window address of the mbarrier
+  uint32_t phase;  // parity of the next completion
+};
+__device__ __forceinline__ void mbar_init(uint32_t mbar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(mbar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
+// Copy tile tau of pass geometry g (2^tb doubles: one contiguous block when g.b == g.c, else
+// 2^(tb-c) runs of 2^c doubles) into the staging buffer.  Called by all threads after a barrier
+// that follows every read of the buffer; generic writes of the source (earlier passes) and reads of
+// the buffer are ordered before the async-proxy copy by fence.proxy.async in each issuing thread.
+template <int TB>
+__device__ __forceinline__ void issue_tile(const Stager& st, const double* __restrict__ base, const Geo& g,
+                                           uint32_t tau, uint32_t t) {
+  constexpr uint32_t TN = 1u << TB, NT = TS<TB>::THREADS;
+  if (g.b == g.c) {
+    constexpr uint32_t CH = 512;  // doubles per request (4 KB)
+    if (t < TN / CH) {
+      asm volatile("fence.proxy.async;" ::: "memory");
+      bulk_g2s(st.buf + t * CH * 8u, base + g.gidx(t * CH, tau), CH * 8u, st.mbar);
+    }
+  } else {
+    const uint32_t runs = 1u << (g.tb - g.c);
+    if (t < runs) asm volatile("fence.proxy.async;" ::: "memory");
+    for (uint32_t u = t; u < runs; u += NT)
+      bulk_g2s(st.buf + (u << g.c) * 8u, base + g.gidx(u << g.c, tau), 8u << g.c, st.mbar);
+  }
+  if (t == 0) mbar_expect(st.mbar, TN * 8u);
+}
+
+// wait for the staged tile, read it into registers in layout S, release the buffer
+template <int S>
+__device__ __forceinline__ void stage_load(double (&v)[16], Stager& st, uint32_t t) {
+  mbar_wait(st.mbar, st.phase);
+  st.phase ^= 1u;
+  const uint32_t a = st.buf + stream::lelem<S>(t, 0) * 8u;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = lds(a + stream::lelem<S>(0, uint32_t(r)) * 8u);
+  __syncthreads();  // every thread has read the buffer: the next copy may overwrite it
+}
+
 // stream::prefetch_tile counts 16-byte amplitudes; a plane tile is half the bytes: prefetch the
 // same index ranges of a double array (the base pointer is reinterpreted; sizes halve)
 __device__ __forceinline__ void prefetch_tile_d(const double* __restrict__ base, const Geo& g, uint32_t tau,
@@ -170,23 +240,37 @@ __device__ __forceinline__ void prefetch_tile_d(const double* __restrict__ base,
   }
 }
 
-template <int TB, int C>
+// STAGED_ mid passes stage only when the tile's contiguous runs are >= 1 KB (c >= 7, n <= 17): TMA
+// copies of 128-512 B runs (n = 18..20) measured no faster than direct register loads + L2 prefetch
+template <int TB, int C, bool STAGED_>
 __device__ __forceinline__ void mid_pass_c(double* __restrict__ phi, uint32_t sm, const Geo& g, int kind, int p,
-                                           uint32_t t0, uint32_t t1, uint32_t t) {
+                                           uint32_t t0, uint32_t t1, uint32_t t, Stager& st) {
+  constexpr bool STAGED = STAGED_ && C >= 7;
   constexpr int lo = C, hi = TB, SH = TS<TB>::SH;
   constexpr bool needLM = lo < 8, needLL = lo < 4;
+  if (STAGED && t0 < t1) issue_tile<TB>(st, phi, g, t0, t);
   for (uint32_t tau = t0; tau < t1; ++tau) {
-    if (tau + 1 < t1) prefetch_tile_d(phi, g, tau + 1, 0u, t, TS<TB>::THREADS);
+    if (!STAGED && tau + 1 < t1) prefetch_tile_d(phi, g, tau + 1, 0u, t, TS<TB>::THREADS);
     double v[16];
+    // STAGED: registers from the staged tile, then the next tile's copy overlaps this one's work
+    auto fetch = [&](auto layout_tag, const auto& cols) {
+      constexpr int S = decltype(layout_tag)::value;
+      if constexpr (STAGED) {
+        stage_load<S>(v, st, t);
+        if (tau + 1 < t1) issue_tile<TB>(st, phi, g, tau + 1, t);
+      } else {
+        gload(v, phi, cols);
+      }
+    };
     if (!needLM) {
       const Cols<SH> cc(g, t, tau);
-      gload(v, phi, cc);
+      fetch(std::integral_constant<int, SH>{}, cc);
       stages<SH, TB>(v, lo, hi);
       if (kind == 1) { zsign(v, cc, p); stages<SH, TB>(v, lo, hi); }
       gstore(v, phi, cc);
     } else if (kind == 2) {
       const Cols<SH> ch(g, t, tau);
-      gload(v, phi, ch);
+      fetch(std::integral_constant<int, SH>{}, ch);
       stages<SH, TB>(v, lo, hi);
       if (needLL) {
         xchg<SH, LL_>(v, sm, t);
@@ -199,7 +283,7 @@ __device__ __forceinline__ void mid_pass_c(double* __restrict__ phi, uint32_t sm
       gstore(v, phi, Cols<LM_>(g, t, tau));
     } else {
       const Cols<LM_> cm(g, t, tau);
-      gload(v, phi, cm);
+      fetch(std::integral_constant<int, LM_>{}, cm);
       stages<LM_, TB>(v, lo, hi);
       if (needLL) {
         xchg<LM_, LL_>(v, sm, t);
@@ -228,20 +312,20 @@ __device__ __forceinline__ void mid_pass_c(double* __restrict__ phi, uint32_t sm
   }
 }
 
-template <int TB>
+template <int TB, bool STAGED>
 __device__ __forceinline__ void mid_pass(double* __restrict__ phi, uint32_t sm, const Geo& g, int kind, int p,
-                                         uint32_t t0, uint32_t t1, uint32_t t) {
+                                         uint32_t t0, uint32_t t1, uint32_t t, Stager& st) {
   switch (g.c) {
-    case 2: mid_pass_c<TB, 2>(phi, sm, g, kind, p, t0, t1, t); break;
-    case 3: mid_pass_c<TB, 3>(phi, sm, g, kind, p, t0, t1, t); break;
-    case 4: mid_pass_c<TB, 4>(phi, sm, g, kind, p, t0, t1, t); break;
-    case 5: mid_pass_c<TB, 5>(phi, sm, g, kind, p, t0, t1, t); break;
-    case 6: mid_pass_c<TB, 6>(phi, sm, g, kind, p, t0, t1, t); break;
-    case 7: mid_pass_c<TB, 7>(phi, sm, g, kind, p, t0, t1, t); break;
-    case 8: mid_pass_c<TB, 8>(phi, sm, g, kind, p, t0, t1, t); break;
-    case 9: mid_pass_c<TB, 9>(phi, sm, g, kind, p, t0, t1, t); break;
-    case 10: mid_pass_c<TB, 10>(phi, sm, g, kind, p, t0, t1, t); break;
-    default: mid_pass_c<TB, 11>(phi, sm, g, kind, p, t0, t1, t); break;
+    case 2: mid_pass_c<TB, 2, STAGED>(phi, sm, g, kind, p, t0, t1, t, st); break;
+    case 3: mid_pass_c<TB, 3, STAGED>(phi, sm, g, kind, p, t0, t1, t, st); break;
+    case 4: mid_pass_c<TB, 4, STAGED>(phi, sm, g, kind, p, t0, t1, t, st); break;
+    case 5: mid_pass_c<TB, 5, STAGED>(phi, sm, g, kind, p, t0, t1, t, st); break;
+    case 6: mid_pass_c<TB, 6, STAGED>(phi, sm, g, kind, p, t0, t1, t, st); break;
+    case 7: mid_pass_c<TB, 7, STAGED>(phi, sm, g, kind, p, t0, t1, t, st); break;
+    case 8: mid_pass_c<TB, 8, STAGED>(phi, sm, g, kind, p, t0, t1, t, st); break;
+    case 9: mid_pass_c<TB, 9, STAGED>(phi, sm, g, kind, p, t0, t1, t, st); break;
+    case 10: mid_pass_c<TB, 10, STAGED>(phi, sm, g, kind, p, t0, t1, t, st); break;
+    default: mid_pass_c<TB, 11, STAGED>(phi, sm, g, kind, p, t0, t1, t, st); break;
   }
 }
 
@@ -266,19 +350,25 @@ __device__ __forceinline__ void first_pass(double* __restrict__ phi, const doubl
 }
 
 // last pass: F2 on tile bits + this plane's readout half
-template <int TB>
+template <int TB, bool STAGED>
 __device__ __forceinline__ double last_pass(const double* __restrict__ phi, const double* __restrict__ xr, uint32_t sm,
                                             const Geo& g0, const PauliTerm& Tl, uint32_t neg, bool big_x,
-                                            uint32_t ntiles, uint32_t t) {
+                                            uint32_t ntiles, uint32_t t, Stager& st) {
   constexpr int SH = TS<TB>::SH;
   double acc = 0.0;
+  if (STAGED) issue_tile<TB>(st, phi, g0, 0, t);
   for (uint32_t tau = 0; tau < ntiles; ++tau) {
     if (tau + 1 < ntiles) {
-      prefetch_tile_d(phi, g0, tau + 1, 0u, t, TS<TB>::THREADS);
+      if (!STAGED) prefetch_tile_d(phi, g0, tau + 1, 0u, t, TS<TB>::THREADS);
       if (big_x) prefetch_tile_d(xr, g0, tau + 1, Tl.xm & ~uint32_t(TS<TB>::TN - 1), t, TS<TB>::THREADS);
     }
     double v[16];
-    gload(v, phi, Cols<SH>(g0, t, tau));
+    if constexpr (STAGED) {
+      stage_load<SH>(v, st, t);
+      if (tau + 1 < ntiles) issue_tile<TB>(st, phi, g0, tau + 1, t);
+    } else {
+      gload(v, phi, Cols<SH>(g0, t, tau));
+    }
     stages<SH, TB>(v, 0, TB);
     xchg<SH, LL_>(v, sm, t);
     stages<LL_, TB>(v, 0, TB);
@@ -292,7 +382,7 @@ __device__ __forceinline__ double last_pass(const double* __restrict__ phi, cons
 // a3-a9 for n >= 11, uniform b: one circuit per CTA at a time, Re plane then Im plane.
 // x_all: planar thetas [K][re 2^n | im 2^n];  scratch: 2^n doubles per CTA (n > TB).
 constexpr int MIN_CTAS = 3;  // CTAs per SM the register budget is sized for (80 registers)
-template <int TB>
+template <int TB, bool STAGED = false>
 __global__ void __launch_bounds__(TS<TB>::THREADS, MIN_CTAS)
 stream_plane_kernel(const double* __restrict__ x_all, const PauliTerm* __restrict__ tab,
                     const double2* __restrict__ coef, int L, int n, int64_t c0, int64_t C,
@@ -316,6 +406,15 @@ stream_plane_kernel(const double* __restrict__ x_all, const PauliTerm* __restric
   const Geo g0 = stream::group(n, 0, TB);
   const bool big_x = n > 22;  // x tiles prefetched too (measured at n = 22: no gain, x of 2 thetas ~ L2)
   if (t == 0) acc4[0] = acc4[1] = acc4[2] = acc4[3] = 0.0;
+  // STAGED: [exchange tile | staging tile | mbarrier] in dynamic SMEM
+  Stager st{sm + uint32_t(tile_smem<TB>()), sm + uint32_t(tile_smem<TB>() + sizeof(double) * (size_t(1) << TB)), 0u};
+  if (STAGED) {
+    if (t == 0) {
+      mbar_init(st.mbar);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
 
   for (int64_t cl = cb; cl < ce; ++cl) {
     const int64_t c = cidx ? cidx[cl] : c0 + cl;
@@ -361,16 +460,16 @@ stream_plane_kernel(const double* __restrict__ x_all, const PauliTerm* __restric
         first_pass<TB>(phi, xpl, sm, g0, Tk, big_x, ntiles, t);
         __syncthreads();
         if (ng == 2) {
-          mid_pass<TB>(phi, sm, stream::group(n, 1, TB), 1, p, 0, ntiles, t);
+          mid_pass<TB, STAGED>(phi, sm, stream::group(n, 1, TB), 1, p, 0, ntiles, t, st);
         } else {
-          mid_pass<TB>(phi, sm, stream::group(n, 1, TB), 0, p, 0, ntiles, t);
+          mid_pass<TB, STAGED>(phi, sm, stream::group(n, 1, TB), 0, p, 0, ntiles, t, st);
           __syncthreads();
-          mid_pass<TB>(phi, sm, stream::group(n, 2, TB), 1, p, 0, ntiles, t);
+          mid_pass<TB, STAGED>(phi, sm, stream::group(n, 2, TB), 1, p, 0, ntiles, t, st);
           __syncthreads();
-          mid_pass<TB>(phi, sm, stream::group(n, 1, TB), 2, p, 0, ntiles, t);
+          mid_pass<TB, STAGED>(phi, sm, stream::group(n, 1, TB), 2, p, 0, ntiles, t, st);
         }
         __syncthreads();
-        acc += last_pass<TB>(phi, xr, sm, g0, Tl, neg, big_x, ntiles, t);
+        acc += last_pass<TB, STAGED>(phi, xr, sm, g0, Tl, neg, big_x, ntiles, t, st);
         __syncthreads();  // scratch reads done before the next plane's / circuit's P0
       }
     }
