@@ -1,0 +1,46 @@
+"""The roofline models bench.py divides by (SURVEY §8(d) "Algorithmic work per circuit" table and
+the streaming model), pinned to the table's printed figures: cfg3 per evaluation 3.54e9 FP64-pipe
+ops and 8.32e9 on-chip bytes (t_FP64 0.190 ms, t_SMEM 0.224 ms at 148 SMs x 1.965 GHz), per-circuit
+43,008 ops / 98,304 B (numerator) and 2,048 ops / 32,768 B (denominator) at n = 10, and the
+streaming DRAM model (64N per numerator circuit while x is L2-resident, x added from n = 22, five
+passes from n = 23).  CPU only."""
+
+import numpy as np
+import pytest
+
+import bench
+from dvqls_inputs import configs
+
+
+def test_cfg3_models_match_survey_table():
+    w = configs.cfg3()
+    ops = bench.fp64_ops_per_eval(w)
+    byts = bench.smem_bytes_per_eval(w)
+    assert abs(ops - 3.54e9) / 3.54e9 < 0.005
+    assert abs(byts - 8.32e9) / 8.32e9 < 0.005
+    assert abs(ops / (64 * 148 * 1.965e9) * 1e3 - 0.190) < 0.001
+    assert abs(byts / (128 * 148 * 1.965e9) * 1e3 - 0.224) < 0.001
+
+
+def test_per_circuit_figures():
+    w = configs.cfg3()
+    num = np.array([2 * 1])           # circuit 2: task 1 = (l=0, k=0, s=1), a numerator
+    den = np.array([0])               # circuit 0: task 0, s = 0, the denominator
+    assert bench.fp64_ops_per_eval(w, num) == 43008
+    assert bench.fp64_ops_per_eval(w, den) == 2048
+    assert bench.smem_bytes_per_eval(w, num) == 98304
+    assert bench.smem_bytes_per_eval(w, den) == 32768
+
+
+@pytest.mark.parametrize("n", [16, 20, 22, 24])
+def test_streaming_dram_model(n):
+    w = configs.cfg5(n)
+    N = 1 << n
+    c = np.arange(w.n_circuits)
+    s = (c // 2) % (n + 1)
+    num, den = int(np.count_nonzero(s)), int(np.count_nonzero(s == 0))
+    per_num = 64 if n <= 21 else (96 if n == 22 else 160)
+    per_den = 0 if n <= 21 else 32
+    assert bench.hbm_bytes_per_eval(w) == num * per_num * N + den * per_den * N
+    # the SURVEY's 96N / 32N figure reported beside it (x counted as HBM at every n)
+    assert bench.smem_bytes_per_eval(w) == num * 96 * N + den * 32 * N
