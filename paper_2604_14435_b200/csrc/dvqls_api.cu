@@ -148,6 +148,7 @@ struct dvqls_ctx {
   int prefix_threads = 0;
   int prefix_rb = 3;
   const void* prefix_fn = nullptr;
+  bool pdl = false;  // Hadamard kernel launched as a programmatic dependent of the prefix
   size_t prefix_smem = 0;
   double hv_scale = 0.0;
 
@@ -308,7 +309,21 @@ int launch_hadamard(dvqls_ctx* ctx, int K, int64_t c0, int64_t C, const int64_t*
                     (void*)&ctx->hv_scale, (void*)&ctx->L, (void*)&c0, (void*)&C, (void*)&K,
                     (void*)&terms, (void*)&ctx->d_partials, (void*)&with_cost, (void*)&red_out,
                     (void*)&ctx->d_counter, (void*)&p2p};
-    CK(cudaLaunchKernel(ctx->kc.fn, dim3(grid), dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
+    if (ctx->pdl) {  // scheduled while the prefix runs; the kernel's griddepcontrol.wait orders the reads
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(grid);
+      lc.blockDim = dim3(ctx->kc.warps * 32);
+      lc.dynamicSmemBytes = ctx->kc.smem;
+      lc.stream = ctx->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      CK(cudaLaunchKernelExC(&lc, ctx->kc.fn, args));
+    } else {
+      CK(cudaLaunchKernel(ctx->kc.fn, dim3(grid), dim3(ctx->kc.warps * 32), args, ctx->kc.smem, ctx->stream));
+    }
   } else if (ctx->onchip) {  // [x_re | -x_re | x_im | -x_im], then the 2-exchange kernel, 1-D grid
     const size_t blk = sizeof(double) * 4 * size_t(ctx->N);  // one theta's x block, a power of two
     double* xq = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ctx->d_xq) + blk - 1) & ~uintptr_t(blk - 1));
@@ -808,6 +823,11 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
   {
     const char* e = getenv("DVQLS_PREFIX_RB");  // tuning knob: register-phase prefix for n <= 10
     ctx->prefix_rb = e ? std::min(std::max(1, std::min(3, atoi(e))), n) : (n <= 10 ? 0 : std::min(3, n));
+  }
+  {  // PDL behind the register prefix (n <= 12, 1-D Hadamard grid); off while the per-kernel
+     // timing events sit between the two launches.  DVQLS_PDL=0 disables it (A/B knob).
+    const char* e = getenv("DVQLS_PDL");
+    ctx->pdl = n <= 12 && !ctx->timing && !(e && e[0] == '0');
   }
   if (n > 12) {
     ctx->prefix_rb = -1;  // global-memory multi-pass prefix (tile.cuh)

@@ -33,6 +33,12 @@ struct PauliTerm {  // P|j> = i^{ny} (-1)^{popcount(j & zm)} |j ^ xm>, big-endia
 // LDS/STS immediate and the per-access address work is a single XOR.
 extern __shared__ double2 dvqls_smem[];
 
+// Programmatic dependent launch (sm_90+): the prefix lets the Hadamard kernel be scheduled while
+// it runs, and the Hadamard kernel waits for the prefix's completion (and memory flush) before it
+// touches anything.  Both are no-ops when the launch does not carry the PDL attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ double2 lds2(uint32_t off) {
   return *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(dvqls_smem) + off);
 }
@@ -66,6 +72,7 @@ __device__ __forceinline__ int pswz(int i) { return i ^ ((i >> 3) & 7); }
 template <int RB>
 __global__ void __launch_bounds__(512)
 prefix_kernel(int n, int layers, int entangler, const double* __restrict__ thetas, double2* __restrict__ x_all) {
+  pdl_trigger();
   constexpr int RA = 1 << RB;
   extern __shared__ double2 psm[];
   const int N = 1 << n;
@@ -190,6 +197,7 @@ __device__ __forceinline__ int tswz(int i) { return i ^ ((i >> 5) & 7); }
 template <int NQ>
 __global__ void __launch_bounds__(1024)
 prefix_lanes_kernel(int layers, int entangler, const double* __restrict__ thetas, double2* __restrict__ x_all) {
+  pdl_trigger();
   constexpr int n = NQ;
   constexpr int N = 1 << n;
   constexpr int LB = n < 5 ? n : 5, WB = n - LB;
@@ -291,6 +299,7 @@ __device__ __forceinline__ int qswz(int i) { return i ^ ((i >> 2) & 7) ^ ((i >> 
 template <int NQ>
 __global__ void __launch_bounds__(256)
 prefix_quad_kernel(int layers, int entangler, const double* __restrict__ thetas, double2* __restrict__ x_all) {
+  pdl_trigger();
   constexpr int n = NQ;
   constexpr int N = 1 << n;
   constexpr int W = n - 7;
@@ -790,6 +799,7 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
                 const double2* __restrict__ coef, const double2* __restrict__ hv, double hv_scale, int L,
                 int64_t c0, int64_t C, int K, double* __restrict__ out_terms, double* __restrict__ partials,
                 int with_cost, double* __restrict__ red_out, unsigned* __restrict__ counter, P2PArgs p2p) {
+  pdl_wait();
   using S = Shape<NQ>;
   constexpr int TB = S::TB, RB = S::RB, GT = S::GT, R = S::R, N = S::N, GPW = S::GPW;
   double2* smem = dvqls_smem;

@@ -94,6 +94,7 @@ plane_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ ta
              double* __restrict__ out_terms, double* __restrict__ partials, int with_cost,
              double* __restrict__ red_out, unsigned* __restrict__ counter, P2PArgs p2p) {
   static_assert(WARPS % 2 == 0 && WARPS / 2 <= 15, "warp pairs use named barriers 1..15");
+  pdl_wait();
   (void)hv; (void)hv_scale;
   constexpr int NP = WARPS / 2;  // circuit groups (warp pairs) per CTA
   constexpr size_t SMALL = small_bytes<WARPS>();
