@@ -12,9 +12,12 @@ evaluates a contiguous 1/N block of the circuits and one NCCL allreduce of
 4 doubles per theta combines them (strong scaling over a fixed workload).
 
 `value` = whole-job circuits/s with theta resident in HBM (device entry point
-dvqls_cost_dev), timed with CUDA events on the library's stream, L2 flushed
-(256 MiB write) before every step, max over ranks.  `e2e` = the same metric
-through the host-buffer C-ABI call dvqls_cost (theta H2D + result D2H inside).
+dvqls_cost_dev, replayed as one CUDA graph per call with the Hadamard kernel launched as a
+programmatic dependent of the prefix), timed with CUDA events on the library's stream, L2
+flushed (256 MiB write) before every step, max over ranks.  `e2e` = the same metric through
+the host-buffer C-ABI call dvqls_cost_batch / dvqls_cost (theta H2D + result D2H inside).
+The per-kernel times behind `roofline` come from a second, identically configured context
+with the library's CUDA events between the kernels (a probe loop in the same run).
 The oracle (oracle/, test infrastructure) is only executed for `cpu_baseline`
 (rank 0, N = 1) and for `--impl reference`.
 """
@@ -160,61 +163,56 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def traffic_from_profiles():
-    p = os.path.join(ROOT, "profiles", "hadamard_dram_traffic.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
-    return None
-
-
 def streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, grid=None):
     b = hbm_bytes_per_eval(w, local_c) * KT
     b96 = smem_bytes_per_eval(w, local_c) * KT
     ach = b / (had_ms * 1e-3)
     peak = float(peaks["hbm_gbs"]) * 1e9
-    plane = w.bkind == 0 and os.environ.get("DVQLS_PLANE", "1") != "0" and os.environ.get("DVQLS_TEAM", "0") != "1"
-    staged = os.environ.get("DVQLS_STAGE", "") != "0" and (w.n >= 16 or os.environ.get("DVQLS_STAGE") == "1")
-    kern = (f"stream_plane_kernel<12, {'TMA-staged' if staged else 'direct'}>" if plane
-            else "stream_hadamard_kernel<12>")
+    plane = w.bkind == 0
+    kern = (f"stream_plane_kernel<12, {'TMA-staged' if w.n >= 16 else 'direct'}>" if plane
+            else "stream_hh_kernel<12>")
     out = {"bound": "hbm", "kernel": kern, "achieved": ach / 1e9, "peak": peak / 1e9,
            "unit": "GB/s", "frac": ach / peak, "traffic": None,
            "model96_GBps": b96 / (had_ms * 1e-3) / 1e9,
            "note": (f"algorithmic DRAM bytes per launch = {b:.4g} (64N per numerator circuit: 3 passes "
                     f"through the per-CTA scratch, x L2-resident; n >= 23: 160N + 32N per denominator) / mean "
                     f"CUDA-event kernel time; peak = hbm_gbs of {peak_src} MEASURED_PEAKS.json. model96_GBps "
-                    f"= the SURVEY §8(d) 96N model (x reads counted as HBM)")}
+                    f"= the SURVEY §8(d) 96N model (x reads counted as HBM); traffic: ncu dram bytes are "
+                    f"in profiles/ (not measured inside this run)")}
     if grid is not None:
-        scratch = grid * (1 << w.n) * (8 if plane else 16)
+        scratch = grid * (1 << w.n) * 8
         out["scratch_bytes"] = scratch
         if scratch <= 100 << 20:
             out["note"] += "; the per-CTA scratch fits in L2 at this n, so L2 bandwidth, not HBM, bounds it"
     return out
 
 
-def onchip_roofline(w, local_c, KT, had_ms, sms, fmax, peak_src):
-    """n = 11, 12 (one tile on chip): FP64-pipe ops vs 64 lanes/clk/SM; on-chip bytes = the SURVEY
-    §8(d) model of the register path (96N per numerator circuit: x read twice + one exchange per
-    FWHT; 32N per denominator), which the default 2-exchange kernel (onchip_plane.cuh) implements
-    (its x reads come from L2 through the L1 pipe).  With DVQLS_ONCHIP=0 the 4-exchange tile
-    kernel runs against the same model."""
+def onchip_roofline(w, local_c, KT, had_ms, sms, fmax, peak_src, kernel):
+    """SMEM-resident paths (n <= 12): the SURVEY §8(d) on-chip model.  FP64-pipe ops ((4n+2)N per
+    numerator circuit, 2N per denominator) against 64 lanes/clk/SM, on-chip bytes (96N per
+    numerator circuit: x read twice + one whole-branch exchange per FWHT; 32N per denominator)
+    against 128 B/clk/SM.  `bound` names the binding one (t_model = max of the two times) and
+    `frac` = t_model / t_kernel, the §8(d) useful-work fraction; the other figure sits beside it."""
     ops = fp64_ops_per_eval(w, local_c) * KT
     sbytes = smem_bytes_per_eval(w, local_c) * KT
     fp64_peak = 64 * sms * fmax
     smem_peak = 128 * sms * fmax
     t = had_ms * 1e-3
-    onchip = w.bkind == 0 and os.environ.get("DVQLS_ONCHIP", "1") != "0" and os.environ.get("DVQLS_PLANE", "1") != "0"
-    kern = (f"onchip_plane_kernel<{w.n}>" if onchip else
-            f"stream_{'plane' if w.bkind == 0 and os.environ.get('DVQLS_PLANE', '1') != '0' else 'hadamard'}_kernel<{11 if w.n == 11 else 12}>")
-    return {"bound": "alu", "kernel": kern,
-            "achieved": ops / t / 1e12, "peak": fp64_peak / 1e12, "unit": "Top/s", "frac": ops / t / fp64_peak,
-            "traffic": None,
-            "smem": {"achieved": sbytes / t / 1e9, "peak": smem_peak / 1e9, "unit": "GB/s",
-                     "frac": sbytes / t / smem_peak,
-                     "note": "on-chip model bytes: 96N per numerator circuit, 32N per denominator"},
+    fp64 = {"achieved": ops / t / 1e12, "peak": fp64_peak / 1e12, "unit": "Top/s", "frac": ops / t / fp64_peak,
+            "note": f"FP64-pipe lane-ops per launch = {ops:.4g} (DADD, DFMA = 1 op each)"}
+    smem = {"achieved": sbytes / t / 1e9, "peak": smem_peak / 1e9, "unit": "GB/s", "frac": sbytes / t / smem_peak,
+            "note": f"on-chip model bytes per launch = {sbytes:.4g} (96N per numerator circuit, 32N per denominator)"}
+    smem_binds = sbytes / smem_peak >= ops / fp64_peak
+    main, other, oname = (smem, fp64, "fp64") if smem_binds else (fp64, smem, "smem")
+    return {"bound": "smem" if smem_binds else "alu", "kernel": kernel,
+            "achieved": main["achieved"], "peak": main["peak"], "unit": main["unit"], "frac": main["frac"],
+            "traffic": None, oname: other,
             "model_frac": max(ops / fp64_peak, sbytes / smem_peak) / t,
-            "note": (f"FP64-pipe lane-ops per launch = {ops:.4g} / mean CUDA-event kernel time; peak = 64 "
-                     f"lanes/clk/SM x {sms} SMs x sm_max_mhz ({peak_src} MEASURED_PEAKS.json)")}
+            "note": (f"{main['note']} / mean CUDA-event time of the kernel on the launching stream (probe "
+                     f"context, same run); peak = {'128 B' if smem_binds else '64 lanes'}/clk/SM x {sms} SMs x "
+                     f"sm_max_mhz ({peak_src} MEASURED_PEAKS.json; per-SM rates confirmed by "
+                     f"tools/microbench.cu, profiles/r1_microbench.json). traffic: ncu dram bytes are in "
+                     f"profiles/ (the kernel reads x, 16 KB per theta, and writes its terms)")}
 
 
 # ----------------------------------------------------------------------------------------------
@@ -273,7 +271,7 @@ def run_reference(args, w):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "circuits/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "n_qubits": w.n, "L": w.L, "layers": w.layers,
                    "circuits_per_eval": w.n_circuits, "sample_circuits_per_step": m},
         "cpu_baseline": {"value": value, "unit": "circuits/s", "cores": cores, "kind": "oracle",
@@ -299,6 +297,9 @@ def main():
     ap.add_argument("--impl", default="dvqls", choices=["dvqls", "reference"])
     ap.add_argument("--slice", type=int, default=0,
                     help="weak-scaling reference (1 GPU only): evaluate rank 0's block of a SLICE-way split")
+    ap.add_argument("--allreduce", default="p2p", choices=["p2p", "nccl"],
+                    help="cross-rank reduction: fused into the kernel tail over NVLink peer memory, or NCCL")
+    ap.add_argument("--no-graphs", action="store_true", help="plain launches instead of one CUDA graph per call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-next2", action="store_true", help="skip the NEXT-2 fast-path side measurement")
     args = ap.parse_args()
@@ -333,17 +334,24 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     KT = args.batch
     chars, co = w.arrays()
-    # device memory comes from torch: the library carves its tables from this workspace
-    if args.slice > 1:
+    vopts = {"allreduce": dvqls.DVQLS_ALLREDUCE_NCCL if args.allreduce == "nccl" else dvqls.DVQLS_ALLREDUCE_P2P,
+             "graphs": not args.no_graphs}
+    if args.slice > 1:  # 1-GPU weak-scaling reference: rank 0's block of a SLICE-way split (virtual rank)
         if world > 1:
             raise SystemExit("--slice is the 1-GPU weak-scaling reference")
-        os.environ["DVQLS_SLICE"] = f"0/{args.slice}"
-    ws_bytes = dvqls.workspace_size(w.n, w.layers, w.L, device=local, rank=rank, world=world,
-                                    max_batch=max(KT, 1))
-    workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    ctx = dvqls.Context(w.n, w.layers, chars, co, w.bkind, w.b, device=local, rank=rank, world=world,
-                        nccl_id=nccl_id, entangler=w.entangler, stream=stream, timing=True,
-                        max_batch=max(KT, 1), workspace=workspace)
+        vopts.update(virtual_rank=0, virtual_world=args.slice)
+
+    def make_ctx(timing):
+        # device memory comes from torch: the library carves its tables from this workspace
+        ws_bytes = dvqls.workspace_size(w.n, w.layers, w.L, device=local, rank=rank, world=world,
+                                        max_batch=max(KT, 1), **{k: v for k, v in vopts.items() if k != "graphs"})
+        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        return dvqls.Context(w.n, w.layers, chars, co, w.bkind, w.b, device=local, rank=rank, world=world,
+                             nccl_id=nccl_id, entangler=w.entangler, stream=stream, timing=timing,
+                             max_batch=max(KT, 1), workspace=workspace, **vopts)
+
+    ctx = make_ctx(False)   # the measured path: CUDA graph per call, PDL between prefix and kernel
+    pctx = make_ctx(True)   # probe: CUDA events between the kernels (per-kernel times, roofline)
     c0, c1 = ctx.local_range()
     thetas = np.stack([w.theta0(s) for s in range(KT)])
     th_dev = torch.tensor(thetas, dtype=torch.float64, device=dev)
@@ -363,94 +371,98 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- device-resident timed region ----------------------------------------------------
-    sampler = ClockSampler(list(range(world))) if rank == 0 else None
-    if sampler:
-        sampler.__enter__()
-    with torch.cuda.stream(stream):
-        # W warm-up steps, continued (in chunks of 8, the same number on every rank: every
-        # call contains a cross-rank reduction) until >= 0.5 s of load so the SM clock has ramped
+    def warm(c, K, min_s=0.5):
+        # W warm-up steps, continued (in chunks of 8, the same number on every rank: every call
+        # contains a cross-rank reduction) until >= min_s of load so the SM clock has ramped
         t_w = time.time()
         i = 0
         while True:
             for _ in range(8):
                 flush.zero_()
-                ctx.cost_dev(KT, th_dev, out_dev)
+                c.cost_dev(K, th_dev, out_dev)
                 i += 1
             torch.cuda.synchronize()
-            more = 1.0 if (i < args.warmup or time.time() - t_w < 0.5) else 0.0
+            more = 1.0 if (i < args.warmup or time.time() - t_w < min_s) else 0.0
             if world > 1:
                 t = torch.tensor([more], device=dev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 more = float(t.item())
             if more == 0.0:
-                break
-        barrier()
-        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+                return
+
+    def timed(c, K, steps, probe=False):
+        """device ms over `steps` calls (events on the library stream around each call), max over
+        ranks; probe: also the library's per-kernel event times of every call"""
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         kt = []
         barrier()
-        if sampler:
-            sampler.start()
-        for i in range(args.steps):
+        for i in range(steps):
             flush.zero_()
             starts[i].record(stream)
-            ctx.cost_dev(KT, th_dev, out_dev)
+            c.cost_dev(K, th_dev, out_dev)
             ends[i].record(stream)
-            kt.append(ctx.last_timings())  # events of the library on the same stream
+            if probe:
+                kt.append(c.last_timings())  # events of the library on the same stream
         barrier()
+        return max_over_ranks(sum(a.elapsed_time(b) for a, b in zip(starts, ends))), kt
+
+    # ---- device-resident timed region (the headline) -----------------------------------------
+    sampler = ClockSampler(list(range(world))) if rank == 0 else None
+    if sampler:
+        sampler.__enter__()
+    with torch.cuda.stream(stream):
+        warm(ctx, KT)
+        if sampler:
+            sampler.start()
+        dev_ms, _ = timed(ctx, KT, args.steps)
         if sampler:
             sampler.stop()
+        # ---- the same loop with a single theta per step (K = 1) --------------------------------
+        k1_steps = max(3, args.steps // 2)
+        warm(ctx, 1, 0.1)
+        k1_ms, _ = timed(ctx, 1, k1_steps)
+        res1 = out_dev[:5].cpu().numpy()
+        warm(ctx, KT, 0.1)
+        ctx.check()
+        res = out_dev.view(KT, 5).cpu().numpy()
+        # ---- probe context: per-kernel CUDA-event times (roofline), K and K = 1 -----------------
+        probe_steps = max(3, args.steps // 4)
+        warm(pctx, KT, 0.2)
+        probe_ms, kt = timed(pctx, KT, probe_steps, probe=True)
+        warm(pctx, 1, 0.05)
+        _, k1t = timed(pctx, 1, probe_steps, probe=True)
     if sampler:
         sampler.__exit__()
-    dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    dev_ms = max_over_ranks(dev_ms)
-
-    # ---- the same timed loop with a single theta per step (K = 1) -------------------------------
-    k1_steps = max(3, args.steps // 2)
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            flush.zero_()
-            ctx.cost_dev(1, th_dev, out_dev)
-        barrier()
-        s1 = [torch.cuda.Event(enable_timing=True) for _ in range(k1_steps)]
-        e1 = [torch.cuda.Event(enable_timing=True) for _ in range(k1_steps)]
-        k1t = []
-        for i in range(k1_steps):
-            flush.zero_()
-            s1[i].record(stream)
-            ctx.cost_dev(1, th_dev, out_dev)
-            e1[i].record(stream)
-            k1t.append(ctx.last_timings())
-        barrier()
-    k1_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in zip(s1, e1)))
-    res1 = out_dev[:5].cpu().numpy()
-    res = out_dev.view(KT, 5).cpu().numpy()
-    if not np.all(np.isfinite(res[:, 0])):
+    if not np.all(np.isfinite(res[:, 0])) and args.slice <= 1:
         print("error: non-finite cost", res, file=sys.stderr)
         return 1
 
-    # ---- end-to-end through the host-buffer C ABI ---------------------------------------------
-    e2e_s = 0.0
-    for _ in range(2):
-        ctx.cost_batch(thetas) if KT > 1 else ctx.cost(thetas[0])
-    barrier()
-    for _ in range(args.steps):
-        with torch.cuda.stream(stream):
-            flush.zero_()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        if KT > 1:
-            ctx.cost_batch(thetas)
-        else:
-            ctx.cost(thetas[0])
-        e2e_s += time.perf_counter() - t0
-    barrier()
-    e2e_s = max_over_ranks(e2e_s)
+    # ---- end-to-end through the host-buffer C ABI (theta H2D + result D2H every step) ----------
+    def e2e_time(K, steps):
+        tot = 0.0
+        for _ in range(2):
+            ctx.cost_batch(thetas[:K]) if K > 1 else ctx.cost(thetas[0])
+        barrier()
+        for _ in range(steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if K > 1:
+                ctx.cost_batch(thetas[:K])
+            else:
+                ctx.cost(thetas[0])
+            tot += time.perf_counter() - t0
+        barrier()
+        return max_over_ranks(tot)
+
+    e2e_s = e2e_time(KT, args.steps)
+    e2e1_s = e2e_time(1, k1_steps)
 
     # ---- NEXT-3 global cost: C_L and C_G of the same call (dvqls_costs_dev) ----------------------
     next3 = None
-    if not args.no_next2:
+    if not args.no_next2 and args.slice <= 1:
         out6 = torch.empty(6 * KT, dtype=torch.float64, device=dev)
         g_steps = max(3, args.steps // 4)
         with torch.cuda.stream(stream):
@@ -497,33 +509,55 @@ def main():
 
     # ---- NEXT-2 algebraic fast path (flagged; reported separately, never the headline) ----------
     next2 = None
-    if w.bkind == 0 and not args.no_next2:
-        pctx = dvqls.Context(w.n, w.layers, chars, co, w.bkind, w.b, device=local, rank=rank, world=world,
+    if w.bkind == 0 and not args.no_next2 and args.slice <= 1:
+        nctx = dvqls.Context(w.n, w.layers, chars, co, w.bkind, w.b, device=local, rank=rank, world=world,
                              nccl_id=nccl_id, entangler=w.entangler, stream=stream, timing=False,
                              max_batch=max(KT, 1), mode=dvqls.DVQLS_MODE_PAULI)
         p_steps = max(3, args.steps // 4)
         with torch.cuda.stream(stream):
             for _ in range(args.warmup):
                 flush.zero_()
-                pctx.cost_dev(KT, th_dev, out_dev)
+                nctx.cost_dev(KT, th_dev, out_dev)
             barrier()
             ps = [torch.cuda.Event(enable_timing=True) for _ in range(p_steps)]
             pe = [torch.cuda.Event(enable_timing=True) for _ in range(p_steps)]
             for i in range(p_steps):
                 flush.zero_()
                 ps[i].record(stream)
-                pctx.cost_dev(KT, th_dev, out_dev)
+                nctx.cost_dev(KT, th_dev, out_dev)
                 pe[i].record(stream)
             barrier()
         p_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in zip(ps, pe)))
         pres = out_dev.view(KT, 5).cpu().numpy()
         next2 = {"evals_per_s": KT * p_steps / (p_ms * 1e-3), "ms_per_step": p_ms / p_steps,
-                 "observables": pctx.num_observables(), "tasks": w.n_tasks,
+                 "observables": nctx.num_observables(), "tasks": w.n_tasks,
                  "max_abs_cost_diff_vs_circuits": float(np.max(np.abs(pres[:, 0] - res[:, 0]))),
                  "note": ("NEXT-2 algebraic fast path (DVQLS_MODE_PAULI): U_b Z_j U_b^+ = X_j, each distinct "
                           "Pauli observable evaluated once per theta, Re/Im shared. Flagged: not circuits/s, "
                           "not the headline (SURVEY §8(d) headline rules)")}
-        pctx.destroy()
+        nctx.destroy()
+
+    # ---- parameter-shift gradient (NEXT-1 with 2P shift points; every circuit simulated) --------
+    grad = None
+    if not args.no_next2 and args.slice <= 1 and w.n <= 12:
+        gout = torch.empty(1 + w.n_params + 4, dtype=torch.float64, device=dev)
+        with torch.cuda.stream(stream):
+            ctx.cost_grad_dev(th_dev[0], gout)
+            barrier()
+            g_steps = 3
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(g_steps):
+                ctx.cost_grad_dev(th_dev[0], gout)
+            e1.record(stream)
+            barrier()
+        gms = max_over_ranks(e0.elapsed_time(e1)) / g_steps
+        rows = 2 * w.n_params + 1
+        grad = {"grads_per_s": 1e3 / gms, "ms_per_grad": gms, "cost_evals_per_grad": rows,
+                "circuits_per_s": rows * w.n_circuits / (gms * 1e-3),
+                "note": (f"dvqls_cost_grad_dev: the 2P = {2 * w.n_params} parameter-shifted thetas + theta, "
+                         f"evaluated in batches of {KT} through the circuit path (one CUDA graph), quotient rule "
+                         "on the device")}
 
     # ---- derived numbers -------------------------------------------------------------------------
     n_eval = (c1 - c0) if args.slice > 1 else w.n_circuits  # circuits this job evaluates per theta
@@ -534,16 +568,17 @@ def main():
     pre_ms = statistics.mean(t["prefix_ms"] for t in kt)
     red_ms = statistics.mean(t["reduce_ms"] for t in kt)
     local_c = np.arange(c0, c1)
-    ops = fp64_ops_per_eval(w, local_c) * KT
-    sbytes = smem_bytes_per_eval(w, local_c) * KT
     peaks, peak_src = load_peaks()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     fmax = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    fp64_peak = 64 * sms * fmax  # FP64 pipe lane-ops/s at max clock
-    smem_peak = 128 * sms * fmax  # B/s at max clock
-    achieved_ops = ops / (had_ms * 1e-3)
-    achieved_smem = sbytes / (had_ms * 1e-3)
     clocks = sampler.summary() if sampler else None
+    if w.n > 12:
+        roof = streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, ctx.grid())
+    else:
+        kern = ("plane_kernel<20>" if w.n == 10 and w.bkind == 0 else
+                f"onchip_plane_kernel<{w.n}>" if w.n > 10 and w.bkind == 0 else
+                "stream_hadamard_kernel<HH>" if w.n > 10 else "hadamard_kernel")
+        roof = onchip_roofline(w, local_c, KT, had_ms, sms, fmax, peak_src, kern)
 
     if rank == 0:
         line = {
@@ -563,44 +598,33 @@ def main():
                 "workload": w.name, "n_qubits": w.n, "L": w.L, "layers": w.layers,
                 "circuits_per_eval": w.n_circuits, "thetas_per_step": KT,
                 "l2": "flushed before every step (256 MiB write, outside the timed events)",
+                "launch": "one CUDA graph per call (prefix -> [PDL] Hadamard kernel with fused reduction)",
                 "parallelism": (f"dp{world} (contiguous circuit blocks; 4 fp64 per theta summed across ranks by the "
                                 "Hadamard kernel's tail over NVLink peer memory, NCCL allreduce as the fallback)"),
-                **({"slice": f"rank 0's block of a {args.slice}-way split ({n_eval} circuits per theta): the "
-                             "1-GPU weak-scaling reference"} if args.slice > 1 else {}),
+                **({"slice": f"rank 0's block of a {args.slice}-way split ({n_eval} circuits per theta, "
+                             "virtual rank): the 1-GPU weak-scaling reference"} if args.slice > 1 else {}),
             },
             "evals_per_s": KT * args.steps / (dev_ms * 1e-3),
             "k1": {"value": n_eval * k1_steps / (k1_ms * 1e-3), "unit": "circuits/s",
                    "ms_per_step": k1_ms / k1_steps, "evals_per_s": k1_steps / (k1_ms * 1e-3),
+                   "e2e": {"value": n_eval * k1_steps / e2e1_s, "unit": "circuits/s",
+                           "h2d_bytes_per_step": 8 * w.n_params, "d2h_bytes_per_step": 8 * 6},
                    "kernel_ms": {"prefix": statistics.mean(t["prefix_ms"] for t in k1t),
                                  "hadamard": statistics.mean(t["hadamard_ms"] for t in k1t),
                                  "reduce": statistics.mean(t["reduce_ms"] for t in k1t)},
                    "note": "one cost evaluation per step (same loop, same L2 flush)"},
-            "kernel_ms": {"prefix": pre_ms, "hadamard": had_ms, "reduce": red_ms},
-            "roofline": streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, ctx.grid()) if w.n > 12 else
-            onchip_roofline(w, local_c, KT, had_ms, sms, fmax, peak_src) if w.n > 10 else {
-                "bound": "alu",
-                "kernel": ("plane_kernel<20>" if w.n == 10 and w.bkind == 0 and os.environ.get("DVQLS_PLANE", "1") != "0"
-                           else "hadamard_kernel"),
-                "achieved": achieved_ops / 1e12,
-                "peak": fp64_peak / 1e12,
-                "unit": "Top/s",
-                "frac": achieved_ops / fp64_peak,
-                "traffic": traffic_from_profiles(),
-                "note": ("FP64-pipe lane-ops (DADD and DFMA = 1 op each; the kernel is >95% DADD) per launch "
-                         f"= {ops:.4g} (SURVEY §8(d)) / mean CUDA-event time of the kernel on the launching "
-                         f"stream; peak = 64 lanes/clk/SM x {sms} SMs x sm_max_mhz ({peak_src} "
-                         "MEASURED_PEAKS.json)"),
-                "smem": {"achieved": achieved_smem / 1e9, "peak": smem_peak / 1e9, "unit": "GB/s",
-                         "frac": achieved_smem / smem_peak,
-                         "note": "on-chip model bytes: 96N per numerator circuit, 32N per denominator"},
-                "model_frac": max(ops / fp64_peak, sbytes / smem_peak) / (had_ms * 1e-3),
-            },
+            "kernel_ms": {"prefix": pre_ms, "hadamard": had_ms, "reduce": red_ms,
+                          "probe_step_ms": probe_ms / probe_steps,
+                          "note": "probe context (CUDA events between the kernels, no graph, no PDL)"},
+            "roofline": roof,
             "e2e": {"value": e2e_value, "unit": "circuits/s", "h2d_bytes_per_step": 8 * w.n_params * KT,
-                    "d2h_bytes_per_step": 40 * KT},
+                    "d2h_bytes_per_step": 8 * (5 * KT + 1)},
             "gpu_launches": args.steps * ctx.launches_per_call(),
+            "graphs": ctx.num_graphs(),
             "clocks": clocks,
             "cost": float(res[0, 0]),
             "cost_k1": float(res1[0]),
+            "shift_grad": grad,
             "next2_pauli": next2,
             "next3_global": next3,
             "next4_decompose": next4,
@@ -608,6 +632,7 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(w, thetas[0])
         print(json.dumps(line), flush=True)
+    pctx.destroy()
     ctx.destroy()
     if world > 1:
         dist.destroy_process_group()

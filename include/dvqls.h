@@ -94,7 +94,42 @@ typedef struct dvqls_opts {
                                   of world > 1 is the one exception: IPC needs its own
                                   allocation).  It must outlive the context.               */
   size_t workspace_bytes;      /* size of workspace_dev                                   */
+  /* ---- fields below: zero selects the default ------------------------------------------- */
+  int virtual_rank;            /* with virtual_world > 1 (and world == 1): evaluate only block
+                                  virtual_rank of a virtual_world-way split of the circuits on
+                                  this one GPU (the sharding of P:394 / SURVEY §8(e) run as one
+                                  virtual rank; the single-GPU weak-scaling reference).  Cost
+                                  calls then return this block's PARTIAL (E, Psi) and C = NaN (no
+                                  DVQLS_E_DEGENERATE); the caller sums the partials in rank order.
+                                  dvqls_terms writes only out[c0, c1).                         */
+  int virtual_world;           /* 0 or 1: off                                                  */
+  int allreduce;               /* world > 1: DVQLS_ALLREDUCE_P2P (0, default): the fused NVLink
+                                  reduction in the Hadamard kernel's tail (falls back to NCCL if a
+                                  peer buffer cannot be mapped and a communicator exists);
+                                  DVQLS_ALLREDUCE_NCCL (1): ncclAllReduce + a finalize kernel     */
+  int p2p_timeout_ms;          /* fused reduction: how long a rank waits for its peers (0 =
+                                  60000).  On expiry the call returns DVQLS_E_NCCL and the context
+                                  refuses further evaluations (destroy and recreate it).        */
+  int (*host_allgather)(void* user, const void* send, void* recv, size_t bytes);
+                               /* world > 1 WITHOUT nccl_unique_id: the caller's allgather of
+                                  `bytes` bytes per rank (recv = world * bytes, rank order; return 0
+                                  on success), e.g. over torch.distributed/gloo.  Used only at
+                                  create (IPC handles of the fused reduction; every rank must map
+                                  every peer, else DVQLS_E_NCCL) and by dvqls_terms (term slices).
+                                  No NCCL communicator is created; ranks may share one GPU.     */
+  void* host_allgather_user;   /* passed back to host_allgather                                */
+  int graphs;                  /* 0: capture each (K, buffers) launch sequence of the cost path in
+                                  a CUDA graph on first use and replay it (default, only when
+                                  timing == 0 and the reduction is not NCCL); -1: plain launches */
+  int pdl;                     /* 0: programmatic dependent launch of the n <= 10 Hadamard kernel
+                                  behind the prefix (default, timing == 0 only); -1: off       */
+  int stage;                   /* n >= 13 uniform b: TMA staging of streaming tiles. 0 = from
+                                  n = 16 (default), -1 = off, 1 = from n = 13                   */
+  int stream_grid;             /* n >= 11: cap on the CTAs of the streaming kernels (0 = one wave) */
 } dvqls_opts;
+
+#define DVQLS_ALLREDUCE_P2P 0
+#define DVQLS_ALLREDUCE_NCCL 1
 
 typedef struct dvqls_ctx dvqls_ctx;
 
@@ -115,7 +150,7 @@ size_t dvqls_workspace_size(int n_qubits, int layers, int n_terms, const dvqls_o
  * block balances equally) and, for world > 1, create the NCCL
  * communicator.  Collective over all ranks when world > 1.
  *   n_qubits    system qubits n, 1 <= n <= 24 (n <= 10: register path; 11..12: SMEM
- *               tile path; 13..24: global streaming path; amplitude b only for n <= 12)
+ *               tile path; 13..24: global streaming path; both U_b kinds at every n)
  *   layers      ansatz depth d >= 1; theta has P = 3*n*layers doubles
  *   n_terms     L >= 1
  *   pauli_terms L*n characters, row-major (term l at pauli_terms + l*n)
@@ -147,6 +182,26 @@ int dvqls_cost(dvqls_ctx* ctx, const double* theta, double* out_cost, double* ou
  * Degenerate entries get NaN and the call returns DVQLS_E_DEGENERATE. */
 int dvqls_cost_batch(dvqls_ctx* ctx, int K, const double* thetas, double* out_costs,
                      double* out_E_Psi);
+
+/* Parameter-shift gradient (NEXT-1 with 2P shift points; SURVEY §8(c) reading 23): every
+ * parameter enters V(theta) through one exp(-i theta sigma/2), so each Hadamard-test value, and
+ * Re E, Re Psi, satisfy df/dtheta_p = [f(theta + pi/2 e_p) - f(theta - pi/2 e_p)] / 2 exactly;
+ *     dC/dtheta_p = -(dReE_p Re Psi - Re E dRePsi_p) / (2 n Re Psi^2).
+ * The 2P shifted thetas and theta are built on the device and evaluated through the circuit path
+ * in batches of max_batch (every circuit simulated: 2P + 1 cost evaluations per gradient).
+ *   theta      P doubles (host)
+ *   out_cost   1 double: C(theta);  out_grad P doubles;  out_E_Psi NULL or 4 doubles at theta
+ * Returns DVQLS_E_DEGENERATE (NaN outputs) if Re Psi(theta) <= 1e-12. */
+int dvqls_cost_grad(dvqls_ctx* ctx, const double* theta, double* out_cost, double* out_grad, double* out_E_Psi);
+
+/* Device-resident parameter-shift gradient, asynchronous on the context stream.
+ *   theta_dev  P doubles (device);  out_dev 1 + P + 4 doubles (device): C, dC/dtheta[P], E, Psi */
+int dvqls_cost_grad_dev(dvqls_ctx* ctx, const double* theta_dev, double* out_dev);
+
+/* Synchronise the context stream and report asynchronous failures of the _dev calls: returns
+ * DVQLS_E_NCCL if a fused-allreduce peer timed out (the context is then unusable), DVQLS_E_CUDA on
+ * a CUDA error, else DVQLS_OK. */
+int dvqls_check(dvqls_ctx* ctx);
 
 /* Device-resident variant: asynchronous on the context stream, no host sync.
  *   thetas_dev  K*P doubles in device memory
@@ -180,8 +235,10 @@ int dvqls_terms_local_dev(dvqls_ctx* ctx, const double* theta_dev, double* out_d
 int dvqls_state(dvqls_ctx* ctx, const double* theta, double* out_state);
 
 /* Term expectations of a subset of circuits (testing at large n, where evaluating all
- * 2(n+1)L^2 circuits takes minutes).  Synchronous; single-rank contexts evaluate only the
- * listed circuits, multi-rank contexts evaluate all and select.
+ * 2(n+1)L^2 circuits takes minutes).  Synchronous; single-rank contexts of the streaming path
+ * (n >= 13, or Householder b at n = 11, 12) evaluate only the listed circuits (in launches of at
+ * most 4096, from buffers planned in the workspace), other contexts evaluate all and select.
+ * Virtual-rank contexts accept only indices inside their block.
  *   idx   count circuit indices in [0, 2(n+1)L^2), host memory
  *   out   count doubles, out[i] = <Z_anc> of circuit idx[i] */
 int dvqls_terms_subset(dvqls_ctx* ctx, const double* theta, const int64_t* idx, int64_t count, double* out);
@@ -230,6 +287,8 @@ int64_t dvqls_num_observables(const dvqls_ctx* ctx);
  * Returns DVQLS_E_ARG / DVQLS_E_PAULI on bad input. */
 int dvqls_task_observable(int n, const char* pauli_l, const char* pauli_k, int s, uint32_t* x_mask,
                           uint32_t* z_mask, int* phase);
+/* CUDA graphs instantiated so far by this context (one per (K, buffers) of the cost path). */
+int dvqls_num_graphs(const dvqls_ctx* ctx);
 /* Kernel launches per cost evaluation call (prefix + circuits + reduce [+ finalize]). */
 int dvqls_launches_per_call(const dvqls_ctx* ctx);
 /* With opts.timing: device milliseconds of the last call, measured with CUDA events

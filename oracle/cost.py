@@ -72,3 +72,39 @@ def global_cost(overlaps: np.ndarray, coeffs, Psi: complex) -> float:
     if Psi.real <= 1e-12:
         raise DegenerateDenominator(f"Re Psi = {Psi.real} <= 1e-12")
     return 1.0 - abs(s) ** 2 / Psi.real
+
+
+def shift_gradient(E_plus, Psi_plus, E_minus, Psi_minus, E0: complex, Psi0: complex, n: int) -> np.ndarray:
+    """Parameter-shift gradient of C (SURVEY §8(c) reading 23; "parameter-shift
+    gradients"), written out step by step.  Every parameter enters V(theta) through one
+    exp(-i theta sigma/2), so each term f obeys df/dtheta_p = [f(theta + pi/2 e_p) - f(theta -
+    pi/2 e_p)] / 2; Re E and Re Psi are fixed linear combinations of terms (Step 4b), hence
+        dReE_p   = (Re E(theta + pi/2 e_p)   - Re E(theta - pi/2 e_p))   / 2
+        dRePsi_p = (Re Psi(theta + pi/2 e_p) - Re Psi(theta - pi/2 e_p)) / 2
+    and C = 1/2 - Re E / (2 n Re Psi) (Step 4c) by the quotient rule:
+        dC/dtheta_p = -(dReE_p Re Psi - Re E dRePsi_p) / (2 n Re Psi^2).
+    E_plus[p], Psi_plus[p] (E_minus, Psi_minus) are the sums at theta +(-) pi/2 e_p."""
+    if Psi0.real <= 1e-12:
+        raise DegenerateDenominator(f"Re Psi = {Psi0.real} <= 1e-12")
+    P = len(E_plus)
+    g = np.empty(P)
+    for p in range(P):
+        dE = (E_plus[p].real - E_minus[p].real) / 2
+        dPsi = (Psi_plus[p].real - Psi_minus[p].real) / 2
+        g[p] = -(dE * Psi0.real - E0.real * dPsi) / (2 * n * Psi0.real ** 2)
+    return g
+
+
+def workload_gradient(w, theta, terms_fn):
+    """(C, dC/dtheta) of a workload at theta: the 2P shifted term arrays from ``terms_fn(w,
+    theta)`` (the gate-by-gate simulator), aggregated and combined by shift_gradient."""
+    co = coeffs_of(w)
+    C0, E0, Psi0 = cost(terms_fn(w, theta), co, w.n, w.L)
+    Ep, Pp, Em, Pm = [], [], [], []
+    for p in range(len(theta)):
+        e = np.zeros(len(theta))
+        e[p] = np.pi / 2
+        a = aggregate(terms_fn(w, theta + e), co, w.n, w.L)
+        b = aggregate(terms_fn(w, theta - e), co, w.n, w.L)
+        Ep.append(a[0]); Pp.append(a[1]); Em.append(b[0]); Pm.append(b[1])
+    return C0, shift_gradient(Ep, Pp, Em, Pm, E0, Psi0, w.n)

@@ -17,7 +17,10 @@
 //   4. controlled A_k: one controlled X/Y/Z per non-identity factor.
 //   5. numerator tasks (s >= 1): controlled U_b^dagger, controlled Z_j,
 //      controlled U_b (Eq. 4; reading 2).  U_b = H^{(x)n} (uniform)
-//      or the dense Householder completion w(I - 2 v v^+/v^+v) (reading 5).
+//      or the Householder completion U_b = w(I - 2 v v^+/v^+v) (reading 5), applied as the
+//      dense 2^n x 2^n matrix for n <= 12 and, for n > 12 (a dense matrix would take
+//      4^n * 16 B), from its definition as psi -> w (psi - 2 v (v^+ psi) / v^+ v), the same
+//      operator (pinned against the dense matrix in tests/test_oracle_sim.py).
 //   6. controlled A_l (A_l^dagger = A_l for Pauli strings).
 //   7. H(anc); 8. <Z_anc> = sum|psi_{anc=0}|^2 - sum|psi_{anc=1}|^2.
 // Task t = ((l*L + k)*(n+1) + s), s = 0 denominator, s = 1+j numerator j;
@@ -112,8 +115,28 @@ Gate2 Rz(double t) {
 struct Problem {
   int n = 0, layers = 0, L = 0, entangler = 0, bkind = 0;
   std::vector<std::string> paulis;  // L strings of n chars
-  std::vector<cplx> Ub, Ubdg;       // dense U_b, U_b^dagger (amplitude b only)
+  std::vector<cplx> Ub, Ubdg;       // dense U_b, U_b^dagger (amplitude b, dense form)
+  std::vector<cplx> hv;             // Householder v = e_0 - conj(w) b (amplitude b)
+  cplx hw = 1.0;                    // Householder phase w
+  double hvv = 0.0;                 // v^+ v
+  bool dense = true;                // U_b applied as the dense matrix (else from v, w)
 };
+
+// Householder form of the oracle (test hook): 0 = dense for n <= 12, definition form above;
+// 1 = definition form at every n; 2 = dense at every n <= 12
+int g_hh_form = 0;
+
+// controlled U_b (or U_b^dagger) = w (I - 2 v v^+ / v^+ v) on the anc = 1 half, from its
+// definition: psi_1 -> w' (psi_1 - (2 / v^+ v) v (v^+ psi_1)), w' = w (U_b) or conj(w) (U_b^dagger:
+// the reflector is Hermitian).  U_b = w I when v = 0.
+void apply_c_householder(State& psi, const Problem& P, bool dagger) {
+  const size_t N = size_t(1) << P.n;
+  const cplx wf = dagger ? std::conj(P.hw) : P.hw;
+  cplx d = 0;
+  for (size_t i = 0; i < N; ++i) d += std::conj(P.hv[i]) * psi[N + i];
+  const cplx f = P.hvv > 0 ? 2.0 * d / P.hvv : cplx(0, 0);
+  for (size_t i = 0; i < N; ++i) psi[N + i] = wf * (psi[N + i] - f * P.hv[i]);
+}
 
 // V(theta) on system qubits (register qubits offset+0 .. offset+n-1)
 void apply_ansatz(State& psi, int m, int offset, const Problem& P, const double* theta) {
@@ -167,8 +190,10 @@ void apply_controlled_Ub(State& psi, const Problem& P, bool dagger) {
   const int m = P.n + 1;
   if (P.bkind == 0) {
     for (int q = 0; q < P.n; ++q) apply_c1q(psi, m, 0, q + 1, kH);
-  } else {
+  } else if (P.dense) {
     apply_c_dense(psi, P.n, dagger ? P.Ubdg : P.Ub);
+  } else {
+    apply_c_householder(psi, P, dagger);
   }
 }
 
@@ -240,6 +265,11 @@ void build_householder(Problem& P, const double* b_amps) {
   for (size_t i = 0; i < N; ++i) v[i] = (i == 0 ? cplx(1, 0) : cplx(0, 0)) - std::conj(w) * b[i];
   double vv = 0;
   for (size_t i = 0; i < N; ++i) vv += std::norm(v[i]);
+  P.hv = v;
+  P.hw = w;
+  P.hvv = vv;
+  P.dense = g_hh_form == 2 || (g_hh_form == 0 && P.n <= 12);
+  if (!P.dense) return;
   P.Ub.assign(N * N, 0);
   P.Ubdg.assign(N * N, 0);
   for (size_t r = 0; r < N; ++r)
@@ -255,7 +285,8 @@ void build_householder(Problem& P, const double* b_amps) {
 int build_problem(Problem& P, int n, int layers, int L, const char* paulis, int entangler,
                   int bkind, const double* b_amps) {
   if (n < 1 || n > 24 || layers < 1 || L < 1 || !paulis) return -1;
-  if (bkind == 1 && (!b_amps || n > 12)) return -1;
+  if (bkind == 1 && !b_amps) return -1;
+  if (bkind == 1 && g_hh_form == 2 && n > 12) return -1;
   P.n = n; P.layers = layers; P.L = L; P.entangler = entangler; P.bkind = bkind;
   P.paulis.resize(L);
   for (int l = 0; l < L; ++l) {
@@ -353,7 +384,10 @@ int oracle_ub_matrix(int n, int bkind, const double* b_amps, double* out) {
   const size_t N = size_t(1) << n;
   if (bkind == 1) {
     if (n > 12) return -1;
+    const int keep = g_hh_form;
+    g_hh_form = 2;
     build_householder(P, b_amps);
+    g_hh_form = keep;
     for (size_t i = 0; i < N * N; ++i) {
       out[2 * i] = P.Ub[i].real();
       out[2 * i + 1] = P.Ub[i].imag();
@@ -374,5 +408,12 @@ int oracle_ub_matrix(int n, int bkind, const double* b_amps, double* out) {
 }
 
 int oracle_hardware_threads(void) { return int(std::thread::hardware_concurrency()); }
+
+// test hook: form of the Householder U_b (0 auto, 1 definition form, 2 dense); returns the old one
+int oracle_set_householder_form(int form) {
+  const int old = g_hh_form;
+  if (form >= 0 && form <= 2) g_hh_form = form;
+  return old;
+}
 
 }  // extern "C"

@@ -46,6 +46,8 @@ def lib():
             L.oracle_ub_matrix.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp]
             L.oracle_ub_matrix.restype = ctypes.c_int
             L.oracle_hardware_threads.restype = ctypes.c_int
+            L.oracle_set_householder_form.argtypes = [ctypes.c_int]
+            L.oracle_set_householder_form.restype = ctypes.c_int
             L.oracle_overlap_terms.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
                                                ctypes.c_int, ctypes.c_int, dp, dp, ctypes.c_int, dp]
             L.oracle_overlap_terms.restype = ctypes.c_int
@@ -60,6 +62,13 @@ def _dp(a):
 def _interleave(z):
     z = np.ascontiguousarray(z, dtype=np.complex128)
     return z.view(np.float64).copy()
+
+
+def set_householder_form(form: int) -> int:
+    """Test hook: how the oracle applies an amplitude-b U_b (0 = dense matrix for n <= 12, else
+    from the definition w(I - 2vv^+/v^+v); 1 = definition form at every n; 2 = dense).  Returns
+    the previous setting."""
+    return int(lib().oracle_set_householder_form(int(form)))
 
 
 def hardware_threads() -> int:

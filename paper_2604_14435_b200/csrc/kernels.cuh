@@ -4,8 +4,6 @@
 //   hadamard_kernel  a3-a9: every Hadamard-test circuit of the rank's block,
 //                    one circuit per thread group, state in registers, x in SMEM,
 //                    coefficient-weighted partial sums fused in (Alg. 1 4a-4b)
-//   reduce_kernel    a9-a10: fixed-order sum of the partials -> (E, Psi) [-> C]
-//   finalize_kernel  a10 after the NCCL allreduce: C = 1/2 - Re E / (2 n Re Psi)
 //
 // Only the ancilla-|1> branch of each Hadamard test is simulated: every gate
 // after the first ancilla H is controlled on the ancilla (or is U_b / U_b^+
@@ -20,13 +18,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-namespace dvqls {
+#include "types.h"
 
-struct PauliTerm {  // P|j> = i^{ny} (-1)^{popcount(j & zm)} |j ^ xm>, big-endian masks
-  uint32_t xm, zm;
-  int32_t ny;
-  uint32_t wpar;  // bit r = popcount(r & (zm >> TB)) & 1: register-part sign word (host-built)
-};
+namespace dvqls {
 
 // Dynamic shared memory of the Hadamard-test kernel.  Accesses are written as
 // byte offsets from this symbol so the compiler folds the base into the
@@ -430,25 +424,15 @@ prefix_quad_kernel(int layers, int entangler, const double* __restrict__ thetas,
 // ---------------------------------------------------------------------------
 // a9/a10 fused into the Hadamard kernels: the last CTA of a theta to finish (ticket
 // counter) sums the NG partial quadruples in a fixed order and writes (C, E, Psi) or
-// (E, Psi) for the cross-rank allreduce.  Bitwise identical to reduce_kernel's order.
+// (E, Psi) for the cross-rank allreduce.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double cost_of_dev(double ReE, double RePsi, int n) {
-  return RePsi <= 1e-12 ? __longlong_as_double(0x7ff8000000000000ll) : 0.5 - 0.5 * ReE / (double(n) * RePsi);
-}
-
-// Fused cross-rank reduction over NVLink peer memory (replaces ncclAllReduce + finalize
-// on the cost path).  Every rank owns a symmetric buffer, IPC-mapped into all peers:
-//   double   slot[2][world][KB][4]   (E, Psi) written by rank r for theta k
-//   uint64_t flag[2][world][KB]      epoch of that write
-// The buffer half is chosen by epoch parity; a rank can be at most one call ahead of any
-// peer (it cannot finish call e+1 before every peer has published call e+1), so two halves
-// suffice.  A bounded spin (~2 s) turns a missing peer into a NaN cost instead of a hang.
-struct P2PArgs {
-  int world, rank, KB;
-  unsigned long long epoch;
-  char* const* peers;  // world device pointers (peers[rank] = own buffer)
-};
-
+// Fused cross-rank reduction over NVLink peer memory (replaces ncclAllReduce + finalize on the
+// cost path; layout and protocol in types.h P2PArgs).  The buffer half is chosen by epoch
+// parity; a rank can be at most one call ahead of any peer (it cannot finish call e+1 before
+// every peer has published call e+1), so two halves suffice.  The wait is bounded by
+// timeout_ns of %globaltimer (wall clock, independent of the SM clock): on expiry the sticky
+// error word is set (the host returns DVQLS_E_NCCL and refuses further cost calls on the
+// context) and the slot's cost is NaN.
 __device__ __forceinline__ double* p2p_slot(char* base, const P2PArgs& a, int par, int r, int k) {
   return reinterpret_cast<double*>(base) + ((size_t(par) * a.world + r) * a.KB + k) * 4;
 }
@@ -456,24 +440,37 @@ __device__ __forceinline__ unsigned long long* p2p_flag(char* base, const P2PArg
   return reinterpret_cast<unsigned long long*>(base + size_t(2) * a.world * a.KB * 32) +
          (size_t(par) * a.world + r) * a.KB + k;
 }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
-__device__ void p2p_allreduce(const P2PArgs& a, int kth, int n, double e0, double e1, double e2, double e3,
+__device__ __forceinline__ double nan_dev() { return __longlong_as_double(0x7ff8000000000000ll); }
+
+__device__ __forceinline__ double cost_of_dev(double ReE, double RePsi, int n) {
+  return RePsi <= 1e-12 ? nan_dev() : 0.5 - 0.5 * ReE / (double(n) * RePsi);
+}
+
+static __device__ void p2p_allreduce(const P2PArgs& a, int kth, int n, double e0, double e1, double e2, double e3,
                               double* __restrict__ out) {
-  const int par = int(a.epoch & 1ull);
+  const unsigned long long epoch = a.epochs[kth] + 1ull;
+  a.epochs[kth] = epoch;  // only this thread reduces slot kth in this launch
+  const int par = int(epoch & 1ull);
   for (int q = 0; q < a.world; ++q) {
     volatile double* d = p2p_slot(a.peers[q], a, par, a.rank, kth);
     d[0] = e0; d[1] = e1; d[2] = e2; d[3] = e3;
   }
   __threadfence_system();
   for (int q = 0; q < a.world; ++q) *reinterpret_cast<volatile unsigned long long*>(
-      p2p_flag(a.peers[q], a, par, a.rank, kth)) = a.epoch;
+      p2p_flag(a.peers[q], a, par, a.rank, kth)) = epoch;
   char* mine = a.peers[a.rank];
   bool ok = true;
-  const long long t0 = clock64();
+  const unsigned long long t0 = globaltimer_ns();
   for (int q = 0; q < a.world && ok; ++q) {
     volatile unsigned long long* f = p2p_flag(mine, a, par, q, kth);
-    while (*f != a.epoch) {
-      if (clock64() - t0 > 4000000000ll) { ok = false; break; }
+    while (*f != epoch) {
+      if (globaltimer_ns() - t0 > a.timeout_ns) { ok = false; break; }
     }
   }
   __threadfence_system();
@@ -483,11 +480,15 @@ __device__ void p2p_allreduce(const P2PArgs& a, int kth, int n, double e0, doubl
     s0 += d[0]; s1 += d[1]; s2 += d[2]; s3 += d[3];
   }
   double* o = out + (size_t)kth * 5;
-  o[0] = ok ? cost_of_dev(s0, s2, n) : __longlong_as_double(0x7ff8000000000000ll);
+  if (!ok) {
+    atomicOr(a.err, 1u);
+    s0 = s1 = s2 = s3 = nan_dev();
+  }
+  o[0] = ok ? cost_of_dev(s0, s2, n) : nan_dev();
   o[1] = s0; o[2] = s1; o[3] = s2; o[4] = s3;
 }
 
-__device__ void finish_partials(const double* __restrict__ partials, int64_t NG, int kth, int n, int with_cost,
+static __device__ void finish_partials(const double* __restrict__ partials, int64_t NG, int kth, int n, int with_cost,
                                 double* __restrict__ out, unsigned* __restrict__ counter,
                                 const P2PArgs* p2p = nullptr) {
   __shared__ unsigned s_last;
@@ -516,9 +517,9 @@ __device__ void finish_partials(const double* __restrict__ partials, int64_t NG,
     for (int w = 0; w < nw; ++w) { e0 += sred[0][w]; e1 += sred[1][w]; e2 += sred[2][w]; e3 += sred[3][w]; }
     if (p2p) {
       p2p_allreduce(*p2p, kth, n, e0, e1, e2, e3, out);
-    } else if (with_cost) {
+    } else if (with_cost) {  // 2: partial sums of a virtual rank (no cost)
       double* o = out + (size_t)kth * 5;
-      o[0] = cost_of_dev(e0, e2, n); o[1] = e0; o[2] = e1; o[3] = e2; o[4] = e3;
+      o[0] = with_cost == 2 ? nan_dev() : cost_of_dev(e0, e2, n); o[1] = e0; o[2] = e1; o[3] = e2; o[4] = e3;
     } else {
       double* o = out + (size_t)kth * 4;
       o[0] = e0; o[1] = e1; o[2] = e2; o[3] = e3;
@@ -531,7 +532,7 @@ __device__ void finish_partials(const double* __restrict__ partials, int64_t NG,
 // thetas: partials[k][G][4] holds one fixed-order quadruple per CTA and theta (zero where the CTA
 // did not touch theta).  The last CTA of the grid (ticket) sums each theta's G quadruples in CTA
 // order and writes (C, E, Psi) / (E, Psi), or runs the NVLink allreduce per theta.
-__device__ void finish_all(const double* __restrict__ partials, int G, int K, int n, int with_cost,
+static __device__ void finish_all(const double* __restrict__ partials, int G, int K, int n, int with_cost,
                            double* __restrict__ out, unsigned* __restrict__ counter, const P2PArgs& p2p) {
   __shared__ unsigned s_last;
   __threadfence();
@@ -555,9 +556,9 @@ __device__ void finish_all(const double* __restrict__ partials, int G, int K, in
     if (lane == 0) {
       if (p2p.world > 1) {
         p2p_allreduce(p2p, k, n, a0, a1, a2, a3, out);
-      } else if (with_cost) {
+      } else if (with_cost) {  // 2: partial sums of a virtual rank (no cost)
         double* o = out + size_t(k) * 5;
-        o[0] = cost_of_dev(a0, a2, n); o[1] = a0; o[2] = a1; o[3] = a2; o[4] = a3;
+        o[0] = with_cost == 2 ? nan_dev() : cost_of_dev(a0, a2, n); o[1] = a0; o[2] = a1; o[3] = a2; o[4] = a3;
       } else {
         double* o = out + size_t(k) * 4;
         o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
@@ -953,55 +954,6 @@ hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__
   }
   }  // theta phases
   if (red_out) finish_all(partials, int(G), K, NQ, with_cost, red_out, counter, p2p);
-}
-
-// ---------------------------------------------------------------------------
-// a9/a10: fixed-order reduction of NG partial quadruples per theta.  One CTA
-// per theta, REDUCE_THREADS threads, strided accumulation then a fixed SMEM
-// tree: bitwise deterministic for a given launch configuration.
-// out: with_cost -> 5 doubles (C, ReE, ImE, RePsi, ImPsi), else 4 (E, Psi).
-// ---------------------------------------------------------------------------
-constexpr int REDUCE_THREADS = 256;
-
-__device__ __forceinline__ double cost_of(double ReE, double RePsi, int n) {
-  return RePsi <= 1e-12 ? __longlong_as_double(0x7ff8000000000000ll) : 0.5 - 0.5 * ReE / (double(n) * RePsi);
-}
-
-__global__ void __launch_bounds__(REDUCE_THREADS)
-reduce_kernel(const double* __restrict__ partials, int64_t NG, int n, int with_cost, double* __restrict__ out) {
-  __shared__ double sh[4][REDUCE_THREADS];
-  const double* p = partials + (size_t)blockIdx.x * NG * 4;
-  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-  for (int64_t i = threadIdx.x; i < NG; i += REDUCE_THREADS) {
-    a0 += p[4 * i + 0]; a1 += p[4 * i + 1]; a2 += p[4 * i + 2]; a3 += p[4 * i + 3];
-  }
-  sh[0][threadIdx.x] = a0; sh[1][threadIdx.x] = a1; sh[2][threadIdx.x] = a2; sh[3][threadIdx.x] = a3;
-  __syncthreads();
-  for (int off = REDUCE_THREADS / 2; off >= 1; off >>= 1) {
-    if (threadIdx.x < off)
-      for (int c = 0; c < 4; ++c) sh[c][threadIdx.x] += sh[c][threadIdx.x + off];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    if (with_cost) {
-      double* o = out + (size_t)blockIdx.x * 5;
-      o[0] = cost_of(sh[0][0], sh[2][0], n);
-      o[1] = sh[0][0]; o[2] = sh[1][0]; o[3] = sh[2][0]; o[4] = sh[3][0];
-    } else {
-      double* o = out + (size_t)blockIdx.x * 4;
-      o[0] = sh[0][0]; o[1] = sh[1][0]; o[2] = sh[2][0]; o[3] = sh[3][0];
-    }
-  }
-}
-
-// a10 after the cross-rank allreduce: (E, Psi)[K] -> (C, E, Psi)[K]
-__global__ void finalize_kernel(const double* __restrict__ ep, int K, int n, double* __restrict__ out) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  const double* e = ep + 4 * k;
-  double* o = out + 5 * k;
-  o[0] = cost_of(e[0], e[2], n);
-  o[1] = e[0]; o[2] = e[1]; o[3] = e[2]; o[4] = e[3];
 }
 
 }  // namespace dvqls

@@ -19,9 +19,7 @@
 namespace dvqls {
 namespace pauli {
 
-struct Obs {
-  uint32_t m, z;  // x-mask, z-mask (big-endian index bits)
-};
+// struct Obs (x-mask, z-mask of one distinct observable): types.h
 
 constexpr int WARPS = 8;
 

@@ -539,113 +539,51 @@ stream_hadamard_kernel(const double2* __restrict__ x_all, const PauliTerm* __res
   if (red_out) finish_partials(partials, G, kth, n, with_cost, red_out, counter, p2p.world > 1 ? &p2p : nullptr);
 }
 
-}  // namespace stream
-}  // namespace dvqls
-
-namespace dvqls {
-namespace stream {
-
-// ---------------------------------------------------------------------------------------------
-// Team mode (n >= 15): T co-resident CTAs (cooperative launch) share ONE circuit at a time, each
-// taking a contiguous 1/T of the tiles of every pass, with a team barrier between passes.  Only
-// NT = grid / T branches are in flight, NT * 2^n * 16 B <= ~80 MB, so the scratch traffic of the
-// three passes stays in L2 instead of HBM (the per-CTA kernel above keeps 296 branches in flight:
-// 1.2 GB at n = 18).  Every circuit is still simulated on its own; the T partial readout sums
-// are combined in a fixed order, so results are deterministic for a launch configuration.
-// ---------------------------------------------------------------------------------------------
-
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Barrier of the T CTAs of a team on a monotone counter (target = T * barriers so far).
-// A bounded spin (~10 s at 2 GHz) sets *err and releases every waiter instead of hanging.
-__device__ __forceinline__ void team_sync(unsigned* ctr, unsigned target, unsigned* err) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-    const long long t0 = clock64();
-    while (int(ld_acquire(ctr) - target) < 0) {
-      if (ld_acquire(err)) break;
-      if (clock64() - t0 > 20000000000ll) { atomicExch(err, 1u); break; }
-      __nanosleep(40);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-// cost units of circuits [0, c) of one theta in canonical order: denominator 1, numerator WN
-constexpr int64_t WN = 4;
-__device__ __forceinline__ int64_t cum_cost(int64_t c, int n) {
-  const int64_t P = 2 * int64_t(n + 1), per = 2 + 2 * int64_t(n) * WN;
-  const int64_t q = c / P, r = c % P;
-  return q * per + (r < 2 ? r : 2) + (r > 2 ? (r - 2) * WN : 0);
-}
-// flattened work f in [0, K*Cloc): theta f / Cloc, circuit c0 + f % Cloc
-__device__ __forceinline__ int64_t cum_flat(int64_t f, int64_t c0, int64_t Cloc, int n) {
-  const int64_t th = f / Cloc, base = cum_cost(c0, n);
-  return th * (cum_cost(c0 + Cloc, n) - base) + cum_cost(c0 + f % Cloc, n) - base;
-}
-// smallest f in [0, W] with cum_flat(f) >= target
-__device__ __forceinline__ int64_t split_flat(int64_t target, int64_t W, int64_t c0, int64_t Cloc, int n) {
-  int64_t lo = 0, hi = W;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (cum_flat(mid, c0, Cloc, n) >= target) hi = mid; else lo = mid + 1;
-  }
-  return lo;
-}
-
+// Householder U_b for n > TB (SURVEY §8(c) reading 5; "fixed unitary U_b", P:505 general b):
+// U_b^+ and U_b act on the branch as phi <- phi - s (h^+ phi) h (the phase w cancels, s = 2/h^+h),
+// so a numerator circuit needs only two inner products with h.  phi_0 = c-A_k x is a signed gather
+// of x, which can be re-read instead of stored, so the circuit is three read-only sweeps over the
+// tiles of x and h and no per-circuit scratch exists:
+//   S1: d1 = h^+ phi_0
+//   S2: phi_1 = Z_j (phi_0 - s d1 h),  d2 = h^+ phi_1
+//   S3: <Z_anc> = Re(i^q sum_j conj(x'_j) (phi_1 - s d2 h)_j),  x' = c-A_l x (readout)
+// Every circuit is still simulated on its own (the sweeps recompute its own phi_0, phi_1).
+// Same launch signature as stream_hadamard_kernel (scratch unused); grid (G, K).
 template <int TB>
 __global__ void __launch_bounds__(TS<TB>::THREADS, 2)
-stream_team_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ tab,
-                   const double2* __restrict__ coef, int L, int n, int64_t c0, int64_t Cloc, int K, int T,
-                   double2* __restrict__ scratch, double* __restrict__ out_terms, double* __restrict__ partials,
-                   double* __restrict__ team_acc, unsigned* __restrict__ team_ctr, unsigned* __restrict__ err,
-                   int with_cost, double* __restrict__ red_out, unsigned* __restrict__ counter, P2PArgs p2p) {
-  using TT = TS<TB>;
-  double2* sm = dvqls_smem;
-  __shared__ double red[TT::THREADS / 32];
+stream_hh_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ tab,
+                 const double2* __restrict__ coef, const double2* __restrict__ hv, double hv_scale, int L, int n,
+                 int64_t c0, int64_t C, const int64_t* __restrict__ cidx, double2* __restrict__ scratch,
+                 double* __restrict__ out_terms, double* __restrict__ partials, int with_cost,
+                 double* __restrict__ red_out, unsigned* __restrict__ counter, P2PArgs p2p) {
+  using T = TS<TB>;
+  (void)scratch;
+  __shared__ double red[T::THREADS / 32];
+  __shared__ double bc[2];
   __shared__ double acc4[4];
-  const int NT = gridDim.x / T;
-  const int g = blockIdx.x / T, r = blockIdx.x % T;
+  const int kth = blockIdx.y;
   const uint32_t N = 1u << n;
+  const double2* __restrict__ x = x_all + (size_t)kth * N;
   const uint32_t t = threadIdx.x;
-  const int ng = ngroups(n, TB);
+  const int64_t G = gridDim.x;
+  const int64_t cb = (int64_t)blockIdx.x * C / G, ce = ((int64_t)blockIdx.x + 1) * C / G;
   const uint32_t ntiles = N >> TB;
-  const uint32_t ta = uint32_t(uint64_t(r) * ntiles / T), tb = uint32_t(uint64_t(r + 1) * ntiles / T);
   const Geo g0 = group(n, 0, TB);
-  const bool big_x = n > 22;  // x tiles prefetched too (measured at n = 22: no gain, x of 2 thetas ~ L2)
-  double2* __restrict__ phi = scratch + size_t(g) * N;
-  unsigned* ctr = team_ctr + g;
-  unsigned bars = 0;
-  const bool lead = r == 0 && t == 0;
-
-  // weighted contiguous split of the flattened (theta, circuit) work over the teams
-  const int64_t W = int64_t(K) * Cloc;
-  const int64_t total = cum_flat(W, c0, Cloc, n);
-  const int64_t fb = split_flat(total * g / NT, W, c0, Cloc, n);
-  const int64_t fe = split_flat(total * (g + 1) / NT, W, c0, Cloc, n);
-  if (lead)
-    for (int k = 0; k < K; ++k)
-      for (int q = 0; q < 4; ++q) partials[(size_t(k) * NT + g) * 4 + q] = 0.0;
   if (t == 0) acc4[0] = acc4[1] = acc4[2] = acc4[3] = 0.0;
-  int cur = -1;
-  int parity = 0;
-  for (int64_t f = fb; f < fe; ++f) {
-    const int th = int(f / Cloc);
-    const int64_t cl = f % Cloc, c = c0 + cl;
-    if (th != cur) {
-      if (lead && cur >= 0)
-        for (int q = 0; q < 4; ++q) partials[(size_t(cur) * NT + g) * 4 + q] = acc4[q];
-      if (t == 0) acc4[0] = acc4[1] = acc4[2] = acc4[3] = 0.0;
-      cur = th;
-    }
-    const double2* __restrict__ x = x_all + size_t(th) * N;
+
+  // (re, im) of s * h^+ v summed over the CTA, broadcast to every thread
+  auto hdot = [&](double dr, double di, double& ar, double& ai) {
+    dr = block_sum(dr, red, T::THREADS);
+    di = block_sum(di, red, T::THREADS);
+    if (t == 0) { bc[0] = dr * hv_scale; bc[1] = di * hv_scale; }
+    __syncthreads();
+    ar = bc[0];
+    ai = bc[1];
+    __syncthreads();  // bc / red reusable
+  };
+
+  for (int64_t cl = cb; cl < ce; ++cl) {
+    const int64_t c = cidx ? cidx[cl] : c0 + cl;
     const int64_t tk = c >> 1;
     const int part = int(c & 1);
     const int sidx = int(tk % (n + 1));
@@ -654,79 +592,87 @@ stream_team_kernel(const double2* __restrict__ x_all, const PauliTerm* __restric
     const PauliTerm Tk = tab[k], Tl = tab[l];
     const int q = (Tk.ny + Tl.ny + 3 * part) & 3;
     const bool im = q & 1;
-    double acc;
+    double acc = 0.0;
     if (sidx == 0) {
-      acc = den_pass<TB>(x, g0, Tk, Tl, im, ta, tb, t);
+      acc = den_pass<TB>(x, g0, Tk, Tl, im, 0, ntiles, t);
     } else {
-      const int p = n - 1 - (sidx - 1);
-      first_pass<TB>(phi, x, sm, g0, Tk, big_x, ta, tb, t);
-      team_sync(ctr, unsigned(T) * ++bars, err);
-      if (ng == 2) {
-        mid_pass<TB>(phi, sm, group(n, 1, TB), 1, p, ta, tb, t);
-      } else {
-        mid_pass<TB>(phi, sm, group(n, 1, TB), 0, p, ta, tb, t);
-        team_sync(ctr, unsigned(T) * ++bars, err);
-        mid_pass<TB>(phi, sm, group(n, 2, TB), 1, p, ta, tb, t);
-        team_sync(ctr, unsigned(T) * ++bars, err);
-        mid_pass<TB>(phi, sm, group(n, 1, TB), 2, p, ta, tb, t);
+      const int p = n - 1 - (sidx - 1);  // Z_j bit position, j = s - 1
+      // S1: d1 = h^+ phi_0
+      double dr = 0.0, di = 0.0;
+      for (uint32_t tau = 0; tau < ntiles; ++tau) {
+        const Cols<LM_> cm(g0, t, tau);
+        double2 v[16];
+        gather(v, x, cm, Tk.xm, Tk.zm);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const double2 h = __ldg(at(hv, cm.j(r)));
+          dr = fma(h.x, v[r].x, fma(h.y, v[r].y, dr));
+          di = fma(h.x, v[r].y, fma(-h.y, v[r].x, di));
+        }
       }
-      team_sync(ctr, unsigned(T) * ++bars, err);
-      acc = last_pass<TB>(phi, x, sm, g0, Tl, im, big_x, ta, tb, t);
+      double ar, ai;
+      hdot(dr, di, ar, ai);
+      // S2: phi_1 = Z_j (phi_0 - a h), d2 = h^+ phi_1
+      dr = 0.0;
+      di = 0.0;
+      for (uint32_t tau = 0; tau < ntiles; ++tau) {
+        const Cols<LM_> cm(g0, t, tau);
+        double2 v[16];
+        gather(v, x, cm, Tk.xm, Tk.zm);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const double2 h = __ldg(at(hv, cm.j(r)));
+          v[r].x -= ar * h.x - ai * h.y;
+          v[r].y -= ar * h.y + ai * h.x;
+        }
+        zsign(v, cm, p);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const double2 h = __ldg(at(hv, cm.j(r)));
+          dr = fma(h.x, v[r].x, fma(h.y, v[r].y, dr));
+          di = fma(h.x, v[r].y, fma(-h.y, v[r].x, di));
+        }
+      }
+      double br, bi;
+      hdot(dr, di, br, bi);
+      // S3: readout of phi_1 - b h
+      for (uint32_t tau = 0; tau < ntiles; ++tau) {
+        const Cols<LM_> cm(g0, t, tau);
+        double2 v[16];
+        gather(v, x, cm, Tk.xm, Tk.zm);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const double2 h = __ldg(at(hv, cm.j(r)));
+          v[r].x -= ar * h.x - ai * h.y;
+          v[r].y -= ar * h.y + ai * h.x;
+        }
+        zsign(v, cm, p);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const double2 h = __ldg(at(hv, cm.j(r)));
+          v[r].x -= br * h.x - bi * h.y;
+          v[r].y -= br * h.y + bi * h.x;
+        }
+        acc += readout(v, x, cm, Tl.xm, Tl.zm, im);
+      }
     }
-    const double part_sum = block_sum(acc, red, TT::THREADS);
-    double* slot = team_acc + (size_t(g) * 2 + parity) * T;
-    if (t == 0) slot[r] = part_sum;
-    // all members' sums visible; the scratch is free for the next circuit's P0
-    team_sync(ctr, unsigned(T) * ++bars, err);
-    if (lead) {
-      double val = 0.0;
-      for (int m = 0; m < T; ++m) val += __ldcg(slot + m);  // fixed member order
-      if (sidx > 0) val *= 1.0 / double(N);
-      val = (q == 1 || q == 2) ? -val : val;
-      if (ld_acquire(err)) val = __longlong_as_double(0x7ff8000000000000ll);
-      out_terms[size_t(th) * Cloc + cl] = val;
+    double val = block_sum(acc, red, T::THREADS);
+    if (t == 0) {
+      val = (q == 1 || q == 2) ? -val : val;  // i^q phase: Re(i^q S)
+      out_terms[(size_t)kth * C + cl] = val;
       const double2 cl_ = coef[l], ck = coef[k];
       const double wr = cl_.x * ck.x + cl_.y * ck.y, wi = cl_.x * ck.y - cl_.y * ck.x;
       const double cr = part == 0 ? wr * val : -wi * val;
       const double ci = part == 0 ? wi * val : wr * val;
       if (sidx == 0) { acc4[2] += cr; acc4[3] += ci; } else { acc4[0] += cr; acc4[1] += ci; }
     }
-    parity ^= 1;
+    __syncthreads();  // red reusable by the next circuit
   }
-  if (lead && cur >= 0)
-    for (int q = 0; q < 4; ++q) partials[(size_t(cur) * NT + g) * 4 + q] = acc4[q];
-
-  // ---- a9/a10: the last CTA of the grid sums every theta's NT partials in a fixed order ----
-  __shared__ unsigned s_last;
-  __threadfence();
-  __syncthreads();
-  if (t == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1) ? 1u : 0u;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
   if (t == 0) {
-    const bool bad = ld_acquire(err) != 0;
-    for (int kk = 0; kk < K && red_out; ++kk) {
-      double e0 = 0, e1 = 0, e2 = 0, e3 = 0;
-      for (int gg = 0; gg < NT; ++gg) {
-        const double* pp = partials + (size_t(kk) * NT + gg) * 4;
-        e0 += __ldcg(pp + 0); e1 += __ldcg(pp + 1); e2 += __ldcg(pp + 2); e3 += __ldcg(pp + 3);
-      }
-      if (bad) e2 = __longlong_as_double(0x7ff8000000000000ll);
-      if (p2p.world > 1) {
-        p2p_allreduce(p2p, kk, n, e0, e1, e2, e3, red_out);
-      } else if (with_cost) {
-        double* o = red_out + size_t(kk) * 5;
-        o[0] = cost_of_dev(e0, e2, n); o[1] = e0; o[2] = e1; o[3] = e2; o[4] = e3;
-      } else {
-        double* o = red_out + size_t(kk) * 4;
-        o[0] = e0; o[1] = e1; o[2] = e2; o[3] = e3;
-      }
-    }
-    for (int gg = 0; gg < NT; ++gg) team_ctr[gg] = 0u;  // ready for the next launch
-    *err = 0u;
-    *counter = 0u;
+    double* o = partials + ((size_t)kth * G + blockIdx.x) * 4;
+    o[0] = acc4[0]; o[1] = acc4[1]; o[2] = acc4[2]; o[3] = acc4[3];
   }
+  if (red_out) finish_partials(partials, G, kth, n, with_cost, red_out, counter, p2p.world > 1 ? &p2p : nullptr);
 }
 
 }  // namespace stream

@@ -27,6 +27,8 @@ DVQLS_B_UNIFORM = 0
 DVQLS_B_AMPLITUDES = 1
 DVQLS_MODE_CIRCUITS = 0
 DVQLS_MODE_PAULI = 1
+DVQLS_ALLREDUCE_P2P = 0
+DVQLS_ALLREDUCE_NCCL = 1
 
 EXPORTED = [
     "dvqls_create", "dvqls_destroy", "dvqls_terms", "dvqls_cost", "dvqls_cost_batch",
@@ -35,8 +37,12 @@ EXPORTED = [
     "dvqls_nccl_unique_id", "dvqls_build_info", "dvqls_shard_range", "dvqls_state",
     "dvqls_terms_subset", "dvqls_launch_grid", "dvqls_num_observables", "dvqls_task_observable",
     "dvqls_costs_dev", "dvqls_global_cost", "dvqls_decompose", "dvqls_pauli_coefficients",
-    "dvqls_decompose_error", "dvqls_workspace_size",
+    "dvqls_decompose_error", "dvqls_workspace_size", "dvqls_cost_grad", "dvqls_cost_grad_dev",
+    "dvqls_check", "dvqls_num_graphs",
 ]
+
+# int (*host_allgather)(void* user, const void* send, void* recv, size_t bytes)
+HOST_ALLGATHER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t)
 
 
 class DvqlsError(RuntimeError):
@@ -57,7 +63,50 @@ class _Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
                 ("nccl_unique_id", ctypes.c_void_p), ("entangler", ctypes.c_int),
                 ("cuda_stream", ctypes.c_void_p), ("timing", ctypes.c_int), ("max_batch", ctypes.c_int),
-                ("mode", ctypes.c_int), ("workspace_dev", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
+                ("mode", ctypes.c_int), ("workspace_dev", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
+                ("virtual_rank", ctypes.c_int), ("virtual_world", ctypes.c_int), ("allreduce", ctypes.c_int),
+                ("p2p_timeout_ms", ctypes.c_int), ("host_allgather", HOST_ALLGATHER),
+                ("host_allgather_user", ctypes.c_void_p), ("graphs", ctypes.c_int), ("pdl", ctypes.c_int),
+                ("stage", ctypes.c_int), ("stream_grid", ctypes.c_int)]
+
+
+def _opts(device=-1, rank=0, world=1, nccl_id=None, entangler=0, stream=None, timing=False, max_batch=16, mode=0,
+          workspace=(None, 0), virtual_rank=0, virtual_world=0, allreduce=DVQLS_ALLREDUCE_P2P, p2p_timeout_ms=0,
+          host_allgather=None, graphs=True, pdl=True, stage=0, stream_grid=0):
+    op = _Opts()
+    op.device, op.rank, op.world = int(device), int(rank), int(world)
+    op.nccl_unique_id = nccl_id
+    op.entangler, op.cuda_stream, op.timing = int(entangler), stream, 1 if timing else 0
+    op.max_batch, op.mode = int(max_batch), int(mode)
+    op.workspace_dev, op.workspace_bytes = workspace[0], int(workspace[1])
+    op.virtual_rank, op.virtual_world = int(virtual_rank), int(virtual_world)
+    op.allreduce, op.p2p_timeout_ms = int(allreduce), int(p2p_timeout_ms)
+    if host_allgather is not None:
+        op.host_allgather = host_allgather
+    op.graphs = 0 if graphs else -1
+    op.pdl = 0 if pdl else -1
+    op.stage, op.stream_grid = int(stage), int(stream_grid)
+    return op
+
+
+def make_host_allgather(group=None):
+    """A host_allgather callback over torch.distributed (any backend, e.g. gloo): each rank's
+    `bytes` bytes are gathered in rank order into recv (dvqls_opts.host_allgather)."""
+    import torch.distributed as dist
+
+    def _cb(user, send, recv, nbytes):
+        try:
+            mine = ctypes.string_at(send, nbytes)
+            world = dist.get_world_size(group)
+            out = [None] * world
+            dist.all_gather_object(out, mine, group=group)
+            for r, blob in enumerate(out):
+                ctypes.memmove(recv + r * nbytes, blob, nbytes)
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to the library as a failed exchange
+            return 1
+
+    return HOST_ALLGATHER(_cb)
 
 
 _lib = None
@@ -111,6 +160,10 @@ def load():
     L.dvqls_build_info.restype = ctypes.c_char_p
     L.dvqls_shard_range.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
                                     ctypes.POINTER(ctypes.c_int64)]
+    L.dvqls_cost_grad.argtypes = [vp, dp, dp, dp, dp]
+    L.dvqls_cost_grad_dev.argtypes = [vp, vp, vp]
+    L.dvqls_check.argtypes = [vp]
+    L.dvqls_num_graphs.argtypes = [vp]
     for name in EXPORTED:
         if name not in ("dvqls_destroy", "dvqls_last_error", "dvqls_num_circuits", "dvqls_stream",
                         "dvqls_build_info", "dvqls_num_observables", "dvqls_decompose_error",
@@ -158,10 +211,13 @@ class Context:
 
     def __init__(self, n, layers, paulis: bytes, coeffs, bkind=DVQLS_B_UNIFORM, b=None, device=-1, rank=0,
                  world=1, nccl_id: bytes | None = None, entangler=0, stream=None, timing=False, max_batch=16,
-                 mode=0, workspace=None):
+                 mode=0, workspace=None, **extra):
         """workspace: None (the library allocates its device tables once, here) or caller-owned device
         memory -- a CUDA torch tensor (kept alive by the context) or an (address, bytes) pair -- of at
-        least workspace_size(...) bytes, 256-byte aligned (dvqls_opts.workspace_dev)."""
+        least workspace_size(...) bytes, 256-byte aligned (dvqls_opts.workspace_dev).
+        extra: the remaining dvqls_opts fields by name (virtual_rank, virtual_world, allreduce,
+        p2p_timeout_ms, host_allgather (a HOST_ALLGATHER, see make_host_allgather), graphs, pdl,
+        stage, stream_grid)."""
         L = load()
         self.n, self.layers = int(n), int(layers)
         self.P = 3 * self.n * self.layers
@@ -191,8 +247,10 @@ class Context:
                 self._keep.append(workspace)
             else:
                 wp, wb = int(workspace[0]), int(workspace[1])
-        op = _Opts(device, rank, world, ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None,
-                   entangler, sp, 1 if timing else 0, max_batch, mode, wp, wb)
+        if extra.get("host_allgather") is not None:
+            self._keep.append(extra["host_allgather"])  # the callback must outlive the context
+        op = _opts(device, rank, world, ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None,
+                   entangler, sp, timing, max_batch, mode, (wp, wb), **extra)
         h = ctypes.c_void_p()
         rc = L.dvqls_create(ctypes.byref(h), self.n, self.layers, self.L, paulis, _dp(co), ctypes.byref(bp),
                             ctypes.byref(op))
@@ -202,8 +260,9 @@ class Context:
 
     # --- host-buffer entry points --------------------------------------------
     def terms(self, theta) -> np.ndarray:
+        """All 2(n+1)L^2 terms (a virtual-rank context fills only its block; the rest stays NaN)."""
         th = self._theta(theta, 1)
-        out = np.empty(self.num_circuits(), dtype=np.float64)
+        out = np.full(self.num_circuits(), np.nan, dtype=np.float64)
         _check(load().dvqls_terms(self.h, _dp(th), _dp(out)), self.h)
         return out
 
@@ -235,6 +294,27 @@ class Context:
         ep = np.empty(4 * K)
         _check(load().dvqls_cost_batch(self.h, K, _dp(th), _dp(c), _dp(ep)), self.h)
         return c, ep.reshape(K, 4)
+
+    def cost_grad(self, theta, with_E_Psi=False):
+        """Parameter-shift gradient (dvqls_cost_grad): (C, dC/dtheta[P]) [+ (E, Psi)]."""
+        th = self._theta(theta, 1)
+        c = np.empty(1)
+        g = np.empty(self.P)
+        ep = np.empty(4)
+        _check(load().dvqls_cost_grad(self.h, _dp(th), _dp(c), _dp(g), _dp(ep)), self.h)
+        if with_E_Psi:
+            return float(c[0]), g, complex(ep[0], ep[1]), complex(ep[2], ep[3])
+        return float(c[0]), g
+
+    def cost_grad_dev(self, theta_dev, out_dev):
+        _check(load().dvqls_cost_grad_dev(self.h, _ptr(theta_dev), _ptr(out_dev)), self.h)
+
+    def check(self):
+        """dvqls_check: synchronise and raise on an asynchronous failure (peer timeout)."""
+        _check(load().dvqls_check(self.h), self.h)
+
+    def num_graphs(self) -> int:
+        return int(load().dvqls_num_graphs(self.h))
 
     def terms_subset(self, theta, idx) -> np.ndarray:
         th = self._theta(theta, 1)
@@ -303,9 +383,9 @@ class Context:
 
 
 # C-ABI-named functional wrappers --------------------------------------------------
-def workspace_size(n_qubits, layers, n_terms, device=-1, rank=0, world=1, max_batch=16, mode=0) -> int:
+def workspace_size(n_qubits, layers, n_terms, device=-1, rank=0, world=1, max_batch=16, mode=0, **extra) -> int:
     """dvqls_workspace_size: device bytes a context carves from a caller workspace (0 = invalid)."""
-    op = _Opts(device, rank, world, None, 0, None, 0, max_batch, mode, None, 0)
+    op = _opts(device, rank, world, None, 0, None, False, max_batch, mode, **extra)
     return int(load().dvqls_workspace_size(int(n_qubits), int(layers), int(n_terms), ctypes.byref(op)))
 
 

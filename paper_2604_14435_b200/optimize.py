@@ -7,6 +7,10 @@ gradient are evaluated in ONE batched call (dvqls_cost_batch), so every cost
 evaluation of the loop runs on the GPU path and the launch/allreduce latency is
 amortised over the batch.  Evaluation counts are reported
 in cost evaluations (P+1 per gradient), the unit the paper's budgets use.
+
+gradient="shift" instead takes the exact parameter-shift gradient of the library
+(dvqls_cost_grad: 2P + 1 cost evaluations per gradient, every circuit simulated; P:13,
+SURVEY §8(c) reading 23) as L-BFGS-B's jac.
 """
 
 from __future__ import annotations
@@ -31,10 +35,13 @@ class SolveResult:
 
 
 def solve(ctx: Context, theta0, max_evals: int = 20000, fd_step: float = 1e-8, target_cost: float = 0.0,
-          gtol: float = 1e-12, ftol: float = 1e-16) -> SolveResult:
+          gtol: float = 1e-12, ftol: float = 1e-16, gradient: str = "fd") -> SolveResult:
     P = ctx.P
-    if ctx.max_batch < P + 1:
+    if gradient not in ("fd", "shift"):
+        raise ValueError("gradient must be 'fd' or 'shift'")
+    if gradient == "fd" and ctx.max_batch < P + 1:
         raise ValueError(f"context max_batch={ctx.max_batch} < P+1={P + 1} (needed for batched FD)")
+    per_grad = P + 1 if gradient == "fd" else 2 * P + 1
     evals = [0]
     best = [np.inf, np.asarray(theta0, dtype=np.float64).copy()]
 
@@ -42,6 +49,12 @@ def solve(ctx: Context, theta0, max_evals: int = 20000, fd_step: float = 1e-8, t
         pass
 
     def fun_grad(th):
+        if gradient == "shift":
+            f, g = ctx.cost_grad(th)
+            evals[0] += 2 * P + 1
+            if f < best[0]:
+                best[0], best[1] = f, th.copy()
+            return f, g
         pts = np.repeat(th[None, :], P + 1, axis=0)
         pts[1:] += fd_step * np.eye(P)
         c, _ = ctx.cost_batch(pts)
@@ -61,7 +74,7 @@ def solve(ctx: Context, theta0, max_evals: int = 20000, fd_step: float = 1e-8, t
     try:
         res = minimize(fun_grad, np.asarray(theta0, dtype=np.float64), jac=True, method="L-BFGS-B",
                        bounds=bounds, callback=cb,
-                       options={"maxfun": max(1, max_evals // (P + 1)), "maxiter": 10 ** 6,
+                       options={"maxfun": max(1, max_evals // per_grad), "maxiter": 10 ** 6,
                                 "gtol": gtol, "ftol": ftol, "maxcor": 20})
         msg, nit = str(res.message), int(res.nit)
     except _Stop:

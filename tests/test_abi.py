@@ -44,13 +44,33 @@ def test_built_for_sm100a_only():
     assert not re.search(r"sm_(80|86|89|90)\b", out)
 
 
-def _create(lib, n=2, layers=1, paulis=b"IXZY", coeffs=None, bprep=None):
+def _create(lib, n=2, layers=1, paulis=b"IXZY", coeffs=None, bprep=None, opts=None):
     L = max(1, len(paulis) // max(n, 1))
     co = np.ones(2 * L) if coeffs is None else coeffs
     h = ctypes.c_void_p()
     rc = lib.dvqls_create(ctypes.byref(h), n, layers, L, paulis,
-                          co.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), bprep, None)
+                          co.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), bprep,
+                          ctypes.byref(opts) if opts is not None else None)
     return rc, lib.dvqls_last_error(None).decode()
+
+
+def test_option_errors_without_device(lib):
+    """dvqls_opts fields are validated before any device access (include/dvqls.h)."""
+    rc, msg = _create(lib, opts=dvqls._opts(world=2, rank=0))
+    assert rc == dvqls.DVQLS_E_ARG and "nccl_unique_id or opts.host_allgather" in msg
+    rc, msg = _create(lib, opts=dvqls._opts(world=2, rank=2))
+    assert rc == dvqls.DVQLS_E_ARG and "rank/world" in msg
+    rc, msg = _create(lib, opts=dvqls._opts(virtual_rank=3, virtual_world=3))
+    assert rc == dvqls.DVQLS_E_ARG and "virtual" in msg
+    cb = dvqls.HOST_ALLGATHER(lambda *a: 0)
+    rc, msg = _create(lib, opts=dvqls._opts(world=2, virtual_rank=0, virtual_world=2, host_allgather=cb))
+    assert rc == dvqls.DVQLS_E_ARG and "virtual" in msg
+    rc, msg = _create(lib, opts=dvqls._opts(allreduce=7))
+    assert rc == dvqls.DVQLS_E_ARG and "allreduce" in msg
+    rc, msg = _create(lib, opts=dvqls._opts(world=2, allreduce=dvqls.DVQLS_ALLREDUCE_NCCL, host_allgather=cb))
+    assert rc == dvqls.DVQLS_E_ARG and "NCCL needs" in msg
+    rc, msg = _create(lib, opts=dvqls._opts(mode=5))
+    assert rc == dvqls.DVQLS_E_ARG and "mode" in msg
 
 
 def test_argument_errors_without_device(lib):
@@ -61,7 +81,8 @@ def test_argument_errors_without_device(lib):
     amps[0] = 1.0
     bp13 = dvqls._BPrep(1, amps.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     rc, msg = _create(lib, n=13, paulis=b"I" * 13, bprep=ctypes.byref(bp13))
-    assert rc == dvqls.DVQLS_E_UNSUPPORTED and "n <= 12" in msg
+    # amplitude b is accepted at every n (Householder streaming kernel); what is left is the device
+    assert rc in (dvqls.DVQLS_OK, dvqls.DVQLS_E_CUDA) and "n <= 12" not in msg
     rc, msg = _create(lib, paulis=b"IXQY")
     assert rc == dvqls.DVQLS_E_PAULI and "bad Pauli" in msg
     rc, msg = _create(lib, paulis=b"IXIX")

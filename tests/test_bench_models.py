@@ -44,3 +44,15 @@ def test_streaming_dram_model(n):
     assert bench.hbm_bytes_per_eval(w) == num * per_num * N + den * per_den * N
     # the SURVEY's 96N / 32N figure reported beside it (x counted as HBM at every n)
     assert bench.smem_bytes_per_eval(w) == num * 96 * N + den * 32 * N
+
+
+def test_onchip_roofline_reports_the_binding_model():
+    """cfg3: the SMEM model binds (0.224 vs 0.190 ms per evaluation), so bench.py reports
+    bound = "smem" with frac = t_model / t_kernel and the FP64-pipe fraction beside it."""
+    import numpy as np
+    w = configs.cfg3()
+    lc = np.arange(w.n_circuits)
+    r = bench.onchip_roofline(w, lc, 16, 4.4, 148, 1965e6, "measured", "plane_kernel<20>")
+    assert r["bound"] == "smem" and r["unit"] == "GB/s"
+    assert abs(r["frac"] - r["model_frac"]) < 1e-12
+    assert r["fp64"]["frac"] < r["frac"] and r["traffic"] is None

@@ -1,5 +1,5 @@
-"""GPU parity of the n = 10 real-plane Hadamard-test kernel (csrc/plane.cuh) and of the
-complex-layout kernel it replaced as the default (DVQLS_PLANE=0), both vs the CPU oracle.
+"""GPU parity of the n = 10 real-plane Hadamard-test kernel (csrc/plane.cuh, the headline kernel)
+vs the CPU oracle, and of its launch variants (CUDA-graph replay, programmatic dependent launch).
 
 The plane kernel splits each circuit's branch into Re/Im planes on a warp pair and combines
 the two readout halves every 8 circuits, so the cases below cover: the Im readout path
@@ -8,7 +8,6 @@ counts are not multiples of 8 per pair), a batch of thetas flattened over one gr
 the bitwise determinism of repeated calls.  Tolerance 1e-10 (BASELINE.json north_star).
 """
 
-import os
 
 import numpy as np
 import pytest
@@ -32,23 +31,10 @@ def dv():
     return dvqls
 
 
-def _ctx(dv, w, plane):
-    old = os.environ.get("DVQLS_PLANE")
-    os.environ["DVQLS_PLANE"] = "1" if plane else "0"
-    try:
-        return dv.from_workload(w)
-    finally:
-        if old is None:
-            del os.environ["DVQLS_PLANE"]
-        else:
-            os.environ["DVQLS_PLANE"] = old
-
-
-@pytest.mark.parametrize("plane", [True, False])
 @pytest.mark.parametrize("L,seed", [(3, 1), (5, 2), (7, 3)])
-def test_random_lcu_n10(dv, plane, L, seed):
+def test_random_lcu_n10(dv, L, seed):
     w = configs.random_workload(10, L, 2, seed=200 + seed)
-    ctx = _ctx(dv, w, plane)
+    ctx = dv.from_workload(w)
     try:
         th = w.theta0()
         g = ctx.terms(th)
@@ -61,11 +47,10 @@ def test_random_lcu_n10(dv, plane, L, seed):
         ctx.destroy()
 
 
-@pytest.mark.parametrize("plane", [True, False])
-def test_theta_batch_n10(dv, plane):
+def test_theta_batch_n10(dv):
     """K thetas in one flattened grid: every cost equals the oracle's for its theta."""
     w = configs.random_workload(10, 4, 2, seed=211)
-    ctx = _ctx(dv, w, plane)
+    ctx = dv.from_workload(w)
     try:
         ths = np.stack([w.theta0(s) for s in range(6)])
         cb, _ = ctx.cost_batch(ths)
@@ -77,17 +62,29 @@ def test_theta_batch_n10(dv, plane):
         ctx.destroy()
 
 
-def test_plane_matches_complex_cfg3(dv):
-    """Full cfg3 term array: plane and complex kernels agree to rounding; plane is deterministic."""
+def test_cfg3_launch_variants_bitwise(dv):
+    """Full cfg3: the plain launch sequence, the CUDA-graph replay (default) and the graph without
+    programmatic dependent launch give bitwise identical terms and costs (K = 1 and K = 16)."""
+    import torch
     w = configs.cfg3()
-    th = w.theta0(5)
-    a = _ctx(dv, w, True)
-    b = _ctx(dv, w, False)
+    ths = np.stack([w.theta0(s) for s in range(16)])
+    ctxs = [dv.from_workload(w, graphs=False, pdl=False), dv.from_workload(w), dv.from_workload(w, pdl=False)]
     try:
-        ta, tb = a.terms(th), b.terms(th)
-        assert np.max(np.abs(ta - tb)) <= 1e-12
-        assert np.array_equal(ta, a.terms(th))
-        assert abs(a.cost(th) - b.cost(th)) <= 1e-12
+        th_dev = torch.tensor(ths, dtype=torch.float64, device="cuda")
+        res = []
+        for ctx in ctxs:
+            out = torch.zeros(5 * 16, dtype=torch.float64, device="cuda")
+            for K in (1, 16, 16):
+                ctx.cost_dev(K, th_dev, out)
+            ctx.check()
+            res.append((ctx.terms(ths[3]), out.cpu().numpy(), ctx.cost_batch(ths)[0]))
+        assert ctxs[0].num_graphs() == 0 and ctxs[1].num_graphs() >= 2
+        for r in res[1:]:
+            assert np.array_equal(r[0], res[0][0])
+            assert np.array_equal(r[1], res[0][1])
+            assert np.array_equal(r[2], res[0][2])
+        ref = sim.workload_terms(w, ths[3])
+        assert np.max(np.abs(res[0][0] - ref)) <= TOL
     finally:
-        a.destroy()
-        b.destroy()
+        for ctx in ctxs:
+            ctx.destroy()

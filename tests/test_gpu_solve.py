@@ -1,15 +1,18 @@
-"""GPU: the full D-VQLS loop (BASELINE config 2) - L-BFGS-B on dvqls_cost_batch.
+"""GPU: the full D-VQLS loop - L-BFGS-B on dvqls_cost_batch (BASELINE config 2 and the paper's
+tridiagonal validation, §III-A).
 
-Pin: fidelity F = |<x(theta*)|x*>|^2 > 0.9999 against the classical solution
-x* = A^{-1} b of the same 4x4 Hele-Shaw systems (PAPER.md P:29-31, P:40-52:
-"fidelity results exceeding 0.9999").  Budget 20,000 cost evaluations (SURVEY
-§8(c) reading 22; the paper's 3-4K / 9-10K counts are context).
+Pin: fidelity F = |<x(theta*)|x*>|^2 > 0.9999 against the classical solution x* = A^{-1} b of
+the same system ("fidelity results exceeding 0.9999" for the tridiagonal and
+Hele-Shaw systems).  Budget 20,000 cost evaluations (SURVEY §8(c) reading 22; the paper's ~100 /
+3-4K / 9-10K counts are context, and reading 22 takes the tridiagonal diagonal a in {2.5, 3}
+because (2, -1, -1) stalls under FD L-BFGS-B).  At theta* the oracle's cost equals the GPU's.
 """
 
 import numpy as np
 import pytest
 
 from dvqls_inputs import configs
+from oracle import cost as ocost
 from oracle import sim
 
 pytestmark = pytest.mark.gpu
@@ -37,21 +40,41 @@ def test_state_matches_oracle_ansatz(dv):
             ctx.destroy()
 
 
+def _solve_and_check(dvqls, optimize, w, gradient="fd"):
+    ctx = dvqls.from_workload(w, max_batch=w.n_params + 1)
+    try:
+        res = optimize.solve(ctx, w.theta0(), max_evals=20000, target_cost=1e-10, gradient=gradient)
+        x = ctx.state(res.theta)
+        C_gpu = ctx.cost(res.theta)
+    finally:
+        ctx.destroy()
+    xstar = np.linalg.solve(w.A, w.rhs)
+    F = optimize.fidelity(x, xstar.astype(complex))
+    C_or = ocost.cost(sim.workload_terms(w, res.theta), ocost.coeffs_of(w), w.n, w.L)[0]
+    print(f"{w.name} seed {w.seed} [{gradient}]: C={res.cost:.3e} F={F:.6f} evals={res.n_evals} "
+          f"{res.seconds:.2f}s")
+    assert abs(C_gpu - C_or) <= 1e-10
+    return F
+
+
 @pytest.mark.parametrize("which", ["velocity", "pressure"])
 def test_hele_shaw_converges_to_classical_solution(dv, which):
+    """Config 2: every one of 5 seeds reaches F > 0.9999 (FD gradients, the paper's setting)."""
     dvqls, optimize = dv
     mk = configs.cfg2_velocity if which == "velocity" else configs.cfg2_pressure
-    hits = []
-    for seed in range(5):
-        w = mk(seed)
-        ctx = dvqls.from_workload(w, max_batch=w.n_params + 1)
-        try:
-            res = optimize.solve(ctx, w.theta0(), max_evals=20000, target_cost=1e-10)
-            x = ctx.state(res.theta)
-        finally:
-            ctx.destroy()
-        xstar = np.linalg.solve(w.A, w.rhs)
-        F = optimize.fidelity(x, xstar.astype(complex))
-        hits.append(F > 0.9999)
-        print(f"{w.name} seed {seed}: C={res.cost:.3e} F={F:.6f} evals={res.n_evals} {res.seconds:.2f}s")
-    assert sum(hits) >= 4, hits
+    F = [_solve_and_check(dvqls, optimize, mk(seed)) for seed in range(5)]
+    assert all(f > 0.9999 for f in F), F
+
+
+@pytest.mark.parametrize("a", [2.5, 3.0])
+def test_tridiagonal_converges_to_classical_solution(dv, a):
+    """§III-A validation on the 4-qubit tridiagonal Toeplitz system (diagonal a, off-diagonals -1,
+    uniform b; reading 22), d = 4, seeds 0-2: F > 0.9999 with FD gradients (SciPy's default,
+    reading 20) and with the exact parameter-shift gradient (dvqls_cost_grad)."""
+    dvqls, optimize = dv
+    for seed in range(3):
+        w = configs.tridiag(4, 4, 0.01, seed, a=a)
+        w.name = f"tridiag_a{a}_n4"
+        for gradient in ("fd", "shift"):
+            F = _solve_and_check(dvqls, optimize, w, gradient)
+            assert F > 0.9999, (a, seed, gradient, F)

@@ -1,7 +1,12 @@
-"""GPU parity of the n >= 11 tile path (SMEM tile n <= 12, global streaming n >= 13).
+"""GPU parity of the n >= 11 paths against the gate-by-gate oracle (north_star
+item (3)): the on-chip kernel (n = 11, 12, uniform b), the real-plane streaming kernel (n >= 13,
+uniform b; direct register loads below n = 16, TMA-staged tiles from n = 16) and the Householder
+kernels (amplitude b: one SMEM tile at n = 11, 12, three read-only sweeps from n = 13).
 
-Same bar as the register path: 1e-10 absolute per term and on the cost.  Large n
-use dvqls_terms_subset on evenly strided circuits (config 5 samples).
+Bar: 1e-10 absolute per term and on the cost and (E, Psi) (BASELINE.json north_star).  The
+measured cfg5 configuration is the parameter-shift pair theta +- (pi/2) e_0 through the batched
+path (K = 2, grid (G, K)), so every default kernel is checked there at K = 2 and K = 3, with
+random LCUs whose Pauli masks span all n qubits (not only cfg5's low bits).
 """
 
 import numpy as np
@@ -9,6 +14,7 @@ import pytest
 
 from dvqls_inputs import configs
 from oracle import cost as ocost
+from oracle import dense
 from oracle import sim
 
 pytestmark = pytest.mark.gpu
@@ -25,9 +31,42 @@ def dv():
     return dvqls
 
 
+def _oracle_cost(w, th):
+    return ocost.cost(sim.workload_terms(w, th), ocost.coeffs_of(w), w.n, w.L)
+
+
+def _check_batch(ctx, w, ths):
+    """cost_batch (host buffers) and cost_dev (device buffers, graph-replayed) vs the oracle."""
+    import torch
+    cb, ep = ctx.cost_batch(ths)
+    K = len(ths)
+    th_dev = torch.tensor(ths, dtype=torch.float64, device="cuda")
+    out = torch.zeros(5 * K, dtype=torch.float64, device="cuda")
+    for _ in range(2):  # first call captures the graph, the second replays it
+        ctx.cost_dev(K, th_dev, out)
+        ctx.check()
+    od = out.view(K, 5).cpu().numpy()
+    for k in range(K):
+        Cr, Er, Pr = _oracle_cost(w, ths[k])
+        assert abs(cb[k] - Cr) <= TOL, (k, cb[k], Cr)
+        assert abs(ep[k, 0] - Er.real) <= TOL * max(1.0, abs(Er)) and abs(ep[k, 1] - Er.imag) <= TOL * max(1.0, abs(Er))
+        assert abs(ep[k, 2] - Pr.real) <= TOL * max(1.0, abs(Pr)) and abs(ep[k, 3] - Pr.imag) <= TOL * max(1.0, abs(Pr))
+        assert np.array_equal(od[k], np.concatenate([[cb[k]], ep[k]])), k
+
+
+def _shift_pair(w, p=0):
+    th = w.theta0()
+    pair = np.stack([th, th])
+    pair[0, p] += np.pi / 2
+    pair[1, p] -= np.pi / 2
+    return pair
+
+
 @pytest.mark.parametrize("n,L,amp,ent", [(11, 3, False, 0), (11, 2, True, 0), (12, 3, False, 1),
-                                         (12, 2, True, 0), (13, 2, False, 0), (14, 2, False, 1)])
+                                         (12, 2, True, 0), (13, 2, False, 0), (14, 2, False, 1),
+                                         (13, 2, True, 0), (14, 2, True, 1)])
 def test_full_parity_small_L(dv, n, L, amp, ent):
+    """Every term, C, and V(theta)|0> at n = 11..14 for both U_b kinds."""
     w = configs.random_workload(n, L, 2, seed=50 + n, amplitudes=amp, entangler=ent)
     th = w.theta0()
     ctx = dv.from_workload(w)
@@ -44,9 +83,58 @@ def test_full_parity_small_L(dv, n, L, amp, ent):
         ctx.destroy()
 
 
-@pytest.mark.parametrize("n,nsample", [(12, 96), (14, 48), (16, 24), (18, 12), (20, 6)])
-def test_cfg5_sampled(dv, n, nsample):
-    """Config 5 workload (I^(n-7) (x) pruned tridiag(7), L=64, d=3): strided circuit sample."""
+@pytest.mark.parametrize("n,L,seed", [(13, 3, 1), (14, 2, 2), (15, 2, 3), (16, 2, 4), (17, 2, 5), (18, 2, 6)])
+def test_stream_default_kernel_shift_pair_and_batch(dv, n, L, seed):
+    """The default uniform-b streaming kernel (direct n = 13..15, TMA-staged n >= 16) at K = 2 (the
+    parameter-shift pair of cfg5) and K = 3: cost and (E, Psi) vs the oracle, random LCUs whose
+    masks touch the high qubits (the mid pass's bits)."""
+    w = configs.random_workload(n, L, 1, seed=300 + seed, entangler=seed & 1)
+    masks = [dense.masks(s)[0] | dense.masks(s)[1] for _, s in w.terms]
+    assert any(m >> 12 for m in masks), "LCU should act on the bits above the first tile"
+    ctx = dv.from_workload(w, max_batch=4)
+    try:
+        _check_batch(ctx, w, _shift_pair(w, p=3))
+        _check_batch(ctx, w, np.stack([w.theta0(s) for s in (7, 8, 9)]))
+    finally:
+        ctx.destroy()
+
+
+@pytest.mark.parametrize("n", [14, 16])
+def test_stage_on_off_bitwise(dv, n):
+    """TMA staging changes only where tiles come from: identical terms with opts.stage = 1 / -1."""
+    w = configs.random_workload(n, 2, 1, seed=90 + n)
+    th = w.theta0()
+    a = dv.from_workload(w, stage=1)
+    b = dv.from_workload(w, stage=-1)
+    try:
+        ta, tb = a.terms(th), b.terms(th)
+    finally:
+        a.destroy()
+        b.destroy()
+    assert np.array_equal(ta, tb)
+    assert np.max(np.abs(ta - sim.workload_terms(w, th))) <= TOL
+
+
+@pytest.mark.parametrize("n,L,ent", [(13, 2, 0), (15, 2, 1), (16, 2, 0)])
+def test_householder_stream_shift_pair(dv, n, L, ent):
+    """Amplitude b beyond n = 12 (three read-only sweeps per numerator circuit): full terms at
+    n = 13 and the shift pair + a K = 3 batch vs the oracle (definition-form U_b, reading 5)."""
+    w = configs.random_workload(n, L, 1, seed=600 + n, amplitudes=True, entangler=ent)
+    ctx = dv.from_workload(w, max_batch=4)
+    try:
+        if n == 13:
+            th = w.theta0()
+            assert np.max(np.abs(ctx.terms(th) - sim.workload_terms(w, th))) <= TOL
+        _check_batch(ctx, w, _shift_pair(w, p=1))
+        _check_batch(ctx, w, np.stack([w.theta0(s) for s in (4, 5, 6)]))
+    finally:
+        ctx.destroy()
+
+
+@pytest.mark.parametrize("n,nsample", [(12, 96), (14, 48), (16, 24), (18, 12), (20, 8)])
+def test_cfg5_sampled_subset(dv, n, nsample):
+    """Config 5 workload (I^(n-7) (x) pruned tridiag(7), L=64, d=3): strided circuit sample through
+    dvqls_terms_subset."""
     w = configs.cfg5(n)
     th = w.theta0()
     idx = np.linspace(0, w.n_circuits - 1, nsample).astype(np.int64)
@@ -56,84 +144,86 @@ def test_cfg5_sampled(dv, n, nsample):
         g = ctx.terms_subset(th, idx)
     finally:
         ctx.destroy()
-    ref = sim.workload_terms(w, th, idx=idx)
-    assert np.max(np.abs(g - ref)) <= TOL
+    assert np.max(np.abs(g - sim.workload_terms(w, th, idx=idx))) <= TOL
 
 
-def test_parameter_shift_pair_cost(dv):
-    """Config 5 parameter-shift pair theta +- (pi/2) e_0 at n=12, full cost vs oracle."""
-    w = configs.cfg5(12)
-    th = w.theta0()
-    ctx = dv.from_workload(w)
-    try:
-        pair = np.stack([th, th])
-        pair[0, 0] += np.pi / 2
-        pair[1, 0] -= np.pi / 2
-        cb, _ = ctx.cost_batch(pair)
-    finally:
-        ctx.destroy()
-    idx = None
-    for k in range(2):
-        ref = sim.workload_terms(w, pair[k], idx=idx)
-        Cr = ocost.cost(ref, ocost.coeffs_of(w), w.n, w.L)[0]
-        assert abs(cb[k] - Cr) <= TOL
-
-
-@pytest.mark.parametrize("n,ent", [(15, 0), (16, 1), (17, 0)])
-def test_team_mode_full(dv, n, ent, monkeypatch):
-    """n >= 15 with DVQLS_TEAM=1 runs the team kernel (T CTAs per circuit, cooperative launch): full
-    terms, cost and a batch of 3 thetas against the oracle."""
-    monkeypatch.setenv("DVQLS_TEAM", "1")
-    w = configs.random_workload(n, 2, 2, seed=70 + n, entangler=ent)
-    ctx = dv.from_workload(w, max_batch=4)
-    try:
-        th = w.theta0()
-        g = ctx.terms(th)
-        C = ctx.cost(th)
-        ths = np.stack([w.theta0(s) for s in range(3)])
-        cb, _ = ctx.cost_batch(ths)
-    finally:
-        ctx.destroy()
-    ref = sim.workload_terms(w, th)
-    assert np.max(np.abs(g - ref)) <= TOL
-    assert abs(C - ocost.cost(ref, ocost.coeffs_of(w), w.n, w.L)[0]) <= TOL
-    for k in range(3):
-        rk = sim.workload_terms(w, ths[k])
-        assert abs(cb[k] - ocost.cost(rk, ocost.coeffs_of(w), w.n, w.L)[0]) <= TOL
-
-
-@pytest.mark.parametrize("team", ["0", "1"])
-def test_cfg5_n16_full_sampled(dv, team, monkeypatch):
-    """Config 5 at n = 16, all 139,264 circuits (per-CTA kernel, and the team kernel with
-    DVQLS_TEAM=1), strided sample vs oracle."""
-    monkeypatch.setenv("DVQLS_TEAM", team)
-    w = configs.cfg5(16)
+def test_cfg5_n18_full_launch(dv):
+    """The full cfg5 launch at n = 18 (all 155,648 circuits in one dvqls_terms call: the grid and
+    per-CTA scratch of the measured configuration) against the oracle on a strided sample, and the
+    fused weighted reduction against the oracle's aggregation of the GPU's own terms."""
+    w = configs.cfg5(18)
     th = w.theta0()
     ctx = dv.from_workload(w)
     try:
         g = ctx.terms(th)
+        C, E, Psi = ctx.cost(th, with_E_Psi=True)
     finally:
         ctx.destroy()
-    idx = np.linspace(0, w.n_circuits - 1, 24).astype(np.int64)
+    idx = np.linspace(0, w.n_circuits - 1, 32).astype(np.int64)
     idx[1::2] |= 1
     assert np.max(np.abs(g[idx] - sim.workload_terms(w, th, idx=idx))) <= TOL
+    Ca, Ea, Pa = ocost.cost(g, ocost.coeffs_of(w), w.n, w.L)
+    assert abs(C - Ca) <= 1e-12 and abs(E - Ea) <= 1e-10 and abs(Psi - Pa) <= 1e-10
 
 
-@pytest.mark.parametrize("n,L,ent", [(11, 3, 0), (12, 2, 1), (13, 2, 0), (14, 2, 0)])
-def test_complex_stream_kernel(dv, n, L, ent, monkeypatch):
-    """DVQLS_PLANE=0 keeps the complex-layout streaming kernel (uniform b) selectable: full terms
-    and a batch of two thetas against the oracle (the default above is the real-plane kernel)."""
-    monkeypatch.setenv("DVQLS_PLANE", "0")
-    w = configs.random_workload(n, L, 2, seed=90 + n, entangler=ent)
-    ctx = dv.from_workload(w, max_batch=2)
+_PAR8 = np.array([bin(i).count("1") & 1 for i in range(256)], dtype=np.int8)
+
+
+def _parity(v):
+    p = np.zeros(v.shape, dtype=np.int8)
+    while True:
+        p ^= _PAR8[v & 255]
+        v = v >> 8
+        if not v.any():
+            return p
+
+
+def _closed_form(x, sl, sk, s):
+    """<x|A_l X_j A_k|x> (uniform b: U_b Z_j U_b^+ = X_j) as one Pauli expectation, O(2^n):
+    the string product from oracle/dense.py, the sum with a byte-table parity."""
+    n = len(sl)
+    xj = "".join("X" if q == s - 1 else "I" for q in range(n))
+    ph1, r1 = dense.pauli_product(xj, sk)
+    ph2, r = dense.pauli_product(sl, r1)
+    xm, zm, ny = dense.masks(r)
+    src = np.arange(x.size, dtype=np.int64) ^ xm
+    sign = 1.0 - 2.0 * _parity(src & zm)
+    return ph1 * ph2 * (1j ** ny) * np.sum(np.conj(x) * sign * x[src])
+
+
+def _nontrivial_circuits(w, th, count, rng):
+    """`count` numerator circuits with l != k whose value is not ~0, chosen with the O(2^n) closed
+    form (SURVEY §8(c) pin (ii) for uniform b)."""
+    x = sim.ansatz_state(w.n, w.layers, th, w.entangler)
+    n1, L = w.n + 1, w.L
+    out = []
+    while len(out) < count:
+        l, k = (int(v) for v in rng.integers(0, L, 2))
+        s = int(rng.integers(1, n1))
+        part = int(rng.integers(0, 2))
+        if l == k:
+            continue
+        v = _closed_form(x, w.terms[l][1], w.terms[k][1], s)
+        if abs(v.real if part == 0 else v.imag) < 1e-4:
+            continue
+        c = 2 * ((l * L + k) * n1 + s) + part
+        if c not in out:
+            out.append(c)
+    return np.array(sorted(out), dtype=np.int64)
+
+
+@pytest.mark.parametrize("n", [22, 24])
+def test_cfg5_largest_sizes_sampled(dv, n):
+    """n = 22 and 24, the end of the config-5 sweep: 16 non-trivial numerator circuits (l != k,
+    |value| >= 1e-4) through dvqls_terms_subset vs the gate-by-gate oracle."""
+    w = configs.cfg5(n)
+    th = w.theta0()
+    idx = _nontrivial_circuits(w, th, 16, np.random.default_rng(n))
+    ctx = dv.from_workload(w)
     try:
-        th = w.theta0()
-        g = ctx.terms(th)
-        ths = np.stack([w.theta0(s) for s in range(2)])
-        cb, _ = ctx.cost_batch(ths)
+        g = ctx.terms_subset(th, idx)
     finally:
         ctx.destroy()
-    assert np.max(np.abs(g - sim.workload_terms(w, th))) <= TOL
-    for k in range(2):
-        rk = sim.workload_terms(w, ths[k])
-        assert abs(cb[k] - ocost.cost(rk, ocost.coeffs_of(w), w.n, w.L)[0]) <= TOL
+    ref = sim.workload_terms(w, th, idx=idx)
+    assert np.min(np.abs(ref)) >= 1e-5
+    assert np.max(np.abs(g - ref)) <= TOL

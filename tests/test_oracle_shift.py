@@ -33,20 +33,28 @@ def test_parameter_shift_equals_central_difference(ent):
 
 
 def test_cost_gradient_by_quotient_rule():
-    """dC/dtheta_p from the shifted (E, Psi) pairs: C = 1/2 - Re E / (2 n Re Psi), so
-    dC = -(dReE * RePsi - ReE * dRePsi) / (2 n RePsi^2), against a central difference of C."""
+    """oracle.cost.workload_gradient (parameter shift + quotient rule, reading 23) against a
+    central difference of the oracle's C: a dropped term of the quotient rule, a wrong sign, a
+    missing 1/2 of the shift rule or a permuted parameter index fails at 1e-8."""
     w = configs.cfg1()
     th = w.theta0()
     co = ocost.coeffs_of(w)
-    C0, E0, P0 = ocost.cost(_terms(w, th), co, w.n, w.L)
+    C0, g = ocost.workload_gradient(w, th, _terms)
+    assert abs(C0 - ocost.cost(_terms(w, th), co, w.n, w.L)[0]) == 0.0
     h = 1e-5
-    for p in (0, 7, 23, 47):
+    for p in range(w.n_params):
         e = np.zeros(w.n_params)
         e[p] = 1.0
-        _, Ep, Pp = ocost.cost(_terms(w, th + np.pi / 2 * e), co, w.n, w.L)
-        _, Em, Pm = ocost.cost(_terms(w, th - np.pi / 2 * e), co, w.n, w.L)
-        dE, dP = (Ep.real - Em.real) / 2, (Pp.real - Pm.real) / 2
-        g = -(dE * P0.real - E0.real * dP) / (2 * w.n * P0.real ** 2)
         Cp = ocost.cost(_terms(w, th + h * e), co, w.n, w.L)[0]
         Cm = ocost.cost(_terms(w, th - h * e), co, w.n, w.L)[0]
-        assert abs(g - (Cp - Cm) / (2 * h)) <= 1e-8, p
+        assert abs(g[p] - (Cp - Cm) / (2 * h)) <= 1e-8, p
+
+
+def test_gradient_vanishes_at_the_solution():
+    """At a minimiser of C the gradient is zero: A = I, b = |0>, theta = 0 gives x = b and C = 0
+    (a global minimum of C >= 0), so every dC/dtheta_p = 0 by the shift rule."""
+    n = 2
+    w = configs.Workload("identity_n2", n, 1, [(1.0 + 0j, "II")], configs.B_AMPLITUDES,
+                         np.array([1, 0, 0, 0], complex), 0)
+    C0, g = ocost.workload_gradient(w, np.zeros(w.n_params), _terms)
+    assert abs(C0) < 1e-15 and np.max(np.abs(g)) < 1e-14

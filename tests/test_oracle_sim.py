@@ -178,3 +178,73 @@ def test_pair_conjugacy_and_diagonal_im_zero():
                 assert abs(T[2 * t1 + 1] + T[2 * t2 + 1]) < 1e-13
                 if l == k:
                     assert abs(T[2 * t1 + 1]) < 1e-13
+
+
+# --- Householder U_b in definition form (n > 12; reading 5) ------------------------------------
+
+@pytest.fixture
+def hh_form():
+    old = sim.set_householder_form(1)
+    yield
+    sim.set_householder_form(old)
+
+
+@pytest.mark.parametrize("n,L,ent", [(3, 4, 0), (4, 3, 1), (5, 2, 0)])
+def test_householder_definition_form_matches_dense_quadratic_forms(hh_form, n, L, ent):
+    """The n > 12 form psi -> w(psi - 2 v (v^+ psi)/v^+v) vs the dense quadratic form x^+ B x with
+    B = A_l U_b Z_j U_b^+ A_k built from explicit matrices (dense.py), every circuit."""
+    w = configs.random_workload(n, L, 2, seed=400 + n, amplitudes=True, entangler=ent)
+    th = w.theta0()
+    T = sim.workload_terms(w, th)
+    x = dense.ansatz_state(n, 2, th, ent)
+    assert np.max(np.abs(dense.all_terms_dense(w, x) - T)) < 1e-12
+
+
+def test_householder_definition_form_equals_dense_oracle():
+    """Both oracle forms of the same operator agree to rounding (n = 6, all circuits)."""
+    w = configs.random_workload(6, 3, 2, seed=77, amplitudes=True)
+    th = w.theta0()
+    old = sim.set_householder_form(2)
+    try:
+        a = sim.workload_terms(w, th)
+        sim.set_householder_form(1)
+        b = sim.workload_terms(w, th)
+    finally:
+        sim.set_householder_form(old)
+    assert np.max(np.abs(a - b)) < 1e-13
+
+
+def _pauli_apply(s, x):
+    """(P x)[i] = i^{nY} (-1)^{popcount((i ^ m) & z)} x[i ^ m]  (P|j> = i^{nY} (-1)^{j.z} |j ^ m>)."""
+    xm, zm, ny = dense.masks(s)
+    i = np.arange(x.size)
+    src = i ^ xm
+    return (1j ** ny) * (1.0 - 2.0 * dense._parity(src & zm)) * x[src]
+
+
+@pytest.mark.parametrize("m", [0, 5, 4097])
+def test_householder_large_n_basis_b(m):
+    """n = 13 (definition form by default), b = e_m: w = 1, v = e_0 - e_m, so U_b swaps e_0 and
+    e_m (U_b = I for m = 0) and U_b Z_j U_b^+ is the diagonal sign of Z_j with entries 0 and m
+    exchanged: every term is <A_l x| D_j |A_k x>, an O(2^n) closed form."""
+    n = 13
+    b = np.zeros(1 << n, complex)
+    b[m] = 1.0
+    strings = ["I" * n, "X" + "Y" * 5 + "I" * 6 + "Z", "Z" * 3 + "X" * 10]
+    paulis = "".join(strings).encode()
+    th = seeds.theta0(n, 1, 3)
+    L = len(strings)
+    idx = np.arange(0, 2 * (n + 1) * L * L, 7)
+    T = sim.terms(n, 1, paulis, th, bkind=1, b=b, idx=idx)
+    x = sim.ansatz_state(n, 1, th)
+    i = np.arange(1 << n)
+    for c, v in zip(idx, T):
+        l, k, s, part = _decode(int(c), n, L)
+        yl, yk = _pauli_apply(strings[l], x), _pauli_apply(strings[k], x)
+        if s == 0:
+            d = np.ones(1 << n)
+        else:
+            d = 1.0 - 2.0 * ((i >> (n - s)) & 1)
+            d[[0, m]] = d[[m, 0]]
+        ref = np.vdot(yl, d * yk)
+        assert abs((ref.real if part == 0 else ref.imag) - v) < 1e-12

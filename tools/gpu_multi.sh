@@ -1,17 +1,26 @@
-# multi-GPU iteration: GPU tests (incl. NCCL multirank), bench at N=1 and N=NG via torchrun
-cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out
-TAG=${TAG:-multi}
-NG=$(nvidia-smi -L | wc -l)
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest.log 2>&1
-timeout 300 python bench.py > gpurun_out/${TAG}_bench_n1.json 2> gpurun_out/${TAG}_bench_n1.err
-for N in 2 4 8; do
+# Multi-GPU pass on one box (run with gpurun --gpus N): NCCL/P2P parity (torchrun), strong scaling
+# of cfg3 at 1..N GPUs with the fused NVLink allreduce and with the NCCL fallback, cfg4 at 1 and N.
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out; TAG=${TAG:-m4}
+NG=$(nvidia-smi -L | wc -l); echo "gpus=$NG" > gpurun_out/${TAG}_info.txt
+nvidia-smi topo -m >> gpurun_out/${TAG}_info.txt 2>&1
+timeout 1200 python -m pytest tests/test_multirank.py -x -q > gpurun_out/${TAG}_pytest.log 2>&1
+P=29600
+for N in 1 2 4 8; do
   if [ $N -le $NG ]; then
-    timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 \
-      bench.py --gpus $N > gpurun_out/${TAG}_bench_n$N.json 2> gpurun_out/${TAG}_bench_n$N.err
-    timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29512 \
-      bench.py --gpus $N --batch 16 > gpurun_out/${TAG}_bench_n${N}_k16.json 2> gpurun_out/${TAG}_bench_n${N}_k16.err
+    P=$((P+1))
+    if [ $N -eq 1 ]; then
+      timeout 600 python bench.py --no-cpu-baseline --no-next2 > gpurun_out/${TAG}_cfg3_n1.json 2> gpurun_out/${TAG}_cfg3_n1.err
+    else
+      timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port $P \
+        bench.py --gpus $N --no-next2 > gpurun_out/${TAG}_cfg3_n$N.json 2> gpurun_out/${TAG}_cfg3_n$N.err
+      P=$((P+1))
+      timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
+        --master-port $P bench.py --gpus $N --no-next2 --allreduce nccl > gpurun_out/${TAG}_cfg3_n${N}_nccl.json 2> gpurun_out/${TAG}_cfg3_n${N}_nccl.err
+    fi
   fi
 done
-timeout 300 python bench.py --batch 16 --no-cpu-baseline > gpurun_out/${TAG}_bench_n1_k16.json 2> gpurun_out/${TAG}_bench_n1_k16.err
+timeout 600 python bench.py --config cfg4 --no-cpu-baseline --no-next2 --steps 50 > gpurun_out/${TAG}_cfg4_n1.json 2> gpurun_out/${TAG}_cfg4_n1.err
+P=$((P+1))
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 --master-port $P \
+  bench.py --gpus $NG --config cfg4 --no-next2 --steps 50 > gpurun_out/${TAG}_cfg4_n$NG.json 2> gpurun_out/${TAG}_cfg4_n$NG.err
 echo done
