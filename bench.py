@@ -216,20 +216,31 @@ def onchip_roofline(w, local_c, KT, had_ms, sms, fmax, peak_src, kernel):
 
 
 # ----------------------------------------------------------------------------------------------
-def cpu_baseline(w, theta, budget_s=12.0):
-    """Oracle (as it stands) on all host cores, bounded strided samples of the workload."""
+def _sized_sample(w, theta, mode, cores, target_s):
+    """Evenly strided circuit sample whose oracle run takes ~target_s on `cores` threads: the sample
+    doubles until one run takes >= 1 s, then it is scaled to the target (capped at the workload)."""
+    from oracle import sim
+    m = max(cores, 8)
+    while True:
+        idx = np.linspace(0, w.n_circuits - 1, m).astype(np.int64)
+        t0 = time.perf_counter()
+        sim.workload_terms(w, theta, mode=mode, idx=idx, nthreads=cores)
+        dt = time.perf_counter() - t0
+        if dt >= 1.0 or m >= w.n_circuits:
+            break
+        m = min(w.n_circuits, 2 * m)
+    return int(min(w.n_circuits, max(m, m * target_s / max(dt, 1e-9))))
+
+
+def cpu_baseline(w, theta, target_s=12.0):
+    """Oracle (as it stands) on all host cores, bounded strided samples of the workload (~target_s of
+    CPU work per mode)."""
     from oracle import sim
     cores = sim.hardware_threads()
     out = {"kind": "oracle", "cores": cores, "unit": "circuits/s"}
     res = {}
     for mode, name in ((0, "faithful"), (1, "prefix_shared")):
-        n_probe = max(cores, 8)
-        idx = np.linspace(0, w.n_circuits - 1, n_probe).astype(np.int64)
-        t0 = time.perf_counter()
-        sim.workload_terms(w, theta, mode=mode, idx=idx, nthreads=cores)
-        dt = time.perf_counter() - t0
-        per = dt / n_probe
-        m = int(min(w.n_circuits, max(n_probe, budget_s / 2 / max(per, 1e-9))))
+        m = _sized_sample(w, theta, mode, cores, target_s)
         idx = np.linspace(0, w.n_circuits - 1, m).astype(np.int64)
         t0 = time.perf_counter()
         sim.workload_terms(w, theta, mode=mode, idx=idx, nthreads=cores)

@@ -41,9 +41,13 @@ def test_state_matches_oracle_ansatz(dv):
 
 
 def _solve_and_check(dvqls, optimize, w, gradient="fd"):
-    ctx = dvqls.from_workload(w, max_batch=w.n_params + 1)
+    # same budget of L-BFGS-B gradient calls for both gradients: 20,000 evaluations with FD (P + 1 per
+    # gradient) is 20,000 (2P + 1) / (P + 1) with the parameter shift (2P + 1 per gradient)
+    P = w.n_params
+    budget = 20000 if gradient == "fd" else 20000 * (2 * P + 1) // (P + 1)
+    ctx = dvqls.from_workload(w, max_batch=P + 1)
     try:
-        res = optimize.solve(ctx, w.theta0(), max_evals=20000, target_cost=1e-10, gradient=gradient)
+        res = optimize.solve(ctx, w.theta0(), max_evals=budget, target_cost=1e-10, gradient=gradient)
         x = ctx.state(res.theta)
         C_gpu = ctx.cost(res.theta)
     finally:
@@ -70,7 +74,8 @@ def test_hele_shaw_converges_to_classical_solution(dv, which):
 def test_tridiagonal_converges_to_classical_solution(dv, a):
     """§III-A validation on the 4-qubit tridiagonal Toeplitz system (diagonal a, off-diagonals -1,
     uniform b; reading 22), d = 4, seeds 0-2: F > 0.9999 with FD gradients (SciPy's default,
-    reading 20) and with the exact parameter-shift gradient (dvqls_cost_grad)."""
+    reading 20) and with the exact parameter-shift gradient (dvqls_cost_grad; the same number of
+    gradient calls, i.e. 2P+1 instead of P+1 evaluations each)."""
     dvqls, optimize = dv
     for seed in range(3):
         w = configs.tridiag(4, 4, 0.01, seed, a=a)
