@@ -311,6 +311,7 @@ def main():
     ap.add_argument("--allreduce", default="p2p", choices=["p2p", "nccl"],
                     help="cross-rank reduction: fused into the kernel tail over NVLink peer memory, or NCCL")
     ap.add_argument("--no-graphs", action="store_true", help="plain launches instead of one CUDA graph per call")
+    ap.add_argument("--variant", type=int, default=0, help="n = 10 kernel variant (dvqls_opts.variant)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-next2", action="store_true", help="skip the NEXT-2 fast-path side measurement")
     args = ap.parse_args()
@@ -346,7 +347,7 @@ def main():
     KT = args.batch
     chars, co = w.arrays()
     vopts = {"allreduce": dvqls.DVQLS_ALLREDUCE_NCCL if args.allreduce == "nccl" else dvqls.DVQLS_ALLREDUCE_P2P,
-             "graphs": not args.no_graphs}
+             "graphs": not args.no_graphs, "variant": args.variant}
     if args.slice > 1:  # 1-GPU weak-scaling reference: rank 0's block of a SLICE-way split (virtual rank)
         if world > 1:
             raise SystemExit("--slice is the 1-GPU weak-scaling reference")
@@ -355,7 +356,7 @@ def main():
     def make_ctx(timing):
         # device memory comes from torch: the library carves its tables from this workspace
         ws_bytes = dvqls.workspace_size(w.n, w.layers, w.L, device=local, rank=rank, world=world,
-                                        max_batch=max(KT, 1), **{k: v for k, v in vopts.items() if k != "graphs"})
+                                        max_batch=max(KT, 1), **{k: v for k, v in vopts.items() if k not in ("graphs", "variant")})
         workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         return dvqls.Context(w.n, w.layers, chars, co, w.bkind, w.b, device=local, rank=rank, world=world,
                              nccl_id=nccl_id, entangler=w.entangler, stream=stream, timing=timing,
@@ -586,7 +587,7 @@ def main():
     if w.n > 12:
         roof = streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, ctx.grid())
     else:
-        kern = ("plane_kernel<20>" if w.n == 10 and w.bkind == 0 else
+        kern = (("plane2_kernel" if args.variant == 2 else "plane_kernel<20>") if w.n == 10 and w.bkind == 0 else
                 f"onchip_plane_kernel<{w.n}>" if w.n > 10 and w.bkind == 0 else
                 "stream_hadamard_kernel<HH>" if w.n > 10 else "hadamard_kernel")
         roof = onchip_roofline(w, local_c, KT, had_ms, sms, fmax, peak_src, kern)

@@ -126,6 +126,9 @@ typedef struct dvqls_opts {
   int stage;                   /* n >= 13 uniform b: TMA staging of streaming tiles. 0 = from
                                   n = 16 (default), -1 = off, 1 = from n = 13                   */
   int stream_grid;             /* n >= 11: cap on the CTAs of the streaming kernels (0 = one wave) */
+  int variant;                 /* kernel variant for n = 10, uniform b: 0 = default, 1 = one circuit
+                                  per warp (plane_kernel), 2 = two circuits in flight per warp
+                                  (plane2_kernel).  Same circuits and results to rounding.     */
 } dvqls_opts;
 
 #define DVQLS_ALLREDUCE_P2P 0

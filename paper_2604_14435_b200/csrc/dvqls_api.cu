@@ -553,6 +553,10 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
     fail(ctx, DVQLS_E_ARG, "entangler must be 0 (CNOT ring) or 1 (CZ ring)");
     return bail(DVQLS_E_ARG);
   }
+  if (o.variant < 0 || o.variant > 2) {
+    fail(ctx, DVQLS_E_ARG, "variant must be 0, 1 or 2");
+    return bail(DVQLS_E_ARG);
+  }
   if (o.allreduce != DVQLS_ALLREDUCE_P2P && o.allreduce != DVQLS_ALLREDUCE_NCCL) {
     fail(ctx, DVQLS_E_ARG, "allreduce must be DVQLS_ALLREDUCE_P2P or DVQLS_ALLREDUCE_NCCL");
     return bail(DVQLS_E_ARG);
@@ -652,7 +656,10 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
   }
   if (n <= kMaxRegQubits) {
     ctx->path = Path::reg;
-    ctx->kc = (n == 10 && !hh) ? plane_cfg() : (n <= 6 ? reg_cfg_lo(n, hh) : reg_cfg_hi(n, hh));
+    if (n == 10 && !hh)
+      ctx->kc = o.variant == 2 ? plane2_cfg() : plane_cfg();
+    else
+      ctx->kc = n <= 6 ? reg_cfg_lo(n, hh) : reg_cfg_hi(n, hh);
   } else if (hh) {
     ctx->path = Path::hh_tile;
     ctx->kc = stream_hh_cfg(n);

@@ -6,6 +6,7 @@
 #include "kernels.cuh"
 #include "launch.h"
 #include "plane.cuh"
+#include "plane2.cuh"
 
 namespace dvqls {
 
@@ -25,6 +26,21 @@ KernelCfg plane_cfg() {
   cudaFuncGetAttributes(&fa, k.fn);
   const uint32_t sb = uint32_t(reserved) + ((uint32_t(fa.sharedSizeBytes) + 15u) & ~15u);
   k.smem = plane::smem_bytes<W>(sb);
+  return k;
+}
+
+KernelCfg plane2_cfg() {
+  KernelCfg k;
+  k.fn = (const void*)&plane2::plane2_kernel;
+  k.warps = plane2::WARPS;
+  k.groups = plane2::NP;
+  cudaFuncAttributes fa{};
+  int dev = 0, reserved = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+  cudaFuncGetAttributes(&fa, k.fn);
+  const uint32_t sb = uint32_t(reserved) + ((uint32_t(fa.sharedSizeBytes) + 15u) & ~15u);
+  k.smem = plane2::smem_bytes(sb);
   return k;
 }
 

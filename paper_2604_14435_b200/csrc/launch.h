@@ -15,7 +15,8 @@ KernelCfg reg_cfg_lo(int n, bool householder);
 KernelCfg reg_cfg_hi(int n, bool householder);
 
 // ---- k_plane.cu: the n = 10 uniform-b real-plane kernel (plane.cuh) and the SMEM prefixes
-KernelCfg plane_cfg();  // plane_kernel<20>; SMEM sized for this device's dynamic-SMEM base
+KernelCfg plane_cfg();   // plane_kernel<20>; SMEM sized for this device's dynamic-SMEM base
+KernelCfg plane2_cfg();  // plane2_kernel: two circuits in flight per warp (plane2.cuh)
 // prefix x = V(theta)|0> for n <= 12, one CTA per theta (a2): args (layers, entangler, thetas, x)
 // when !with_n, else (n, layers, entangler, thetas, x)
 struct PrefixCfg {

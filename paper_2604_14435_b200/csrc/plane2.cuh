@@ -1,0 +1,359 @@
+// plane2.cuh - n = 10, uniform-b Hadamard-test kernel, real-plane split (plane.cuh) with TWO
+// circuits in flight per warp, software-pipelined.
+//
+// SURVEY §8(a) a3-a9 for the headline workload, same circuits, gate sequence, data layout and
+// algorithmic work as plane_kernel (plane.cuh; every circuit simulated on its own).  What changes
+// is the instruction stream of a warp.  A numerator circuit alternates SMEM-only phases (gather,
+// two layout exchanges, readout) with FP64-only phases (four 5-stage FWHT blocks), and both
+// resources are needed at ~85 % of their peaks (0.190 vs 0.224 ms per cfg3
+// evaluation), so one circuit per warp leaves them overlapping only as well as the warp
+// scheduler happens to mix warps in different phases.  Here a warp owns two consecutive circuits
+// A, B of the same kind and skews them by one phase, so every code segment pairs one circuit's
+// SMEM phase with the other's FP64 phase:
+//     seg 1: F1(A)           | gather(B)
+//     seg 2: X1(A)           | F1(B)
+//     seg 3: F2 Z F3 (A)     | X1(B)
+//     seg 4: X2(A)           | F2 Z F3 (B)
+//     seg 5: F4(A)           | X2(B)
+//     seg 6: readout(A)      | F4(B)
+//     seg 7: readout(B)
+// (F = five register butterfly stages, X = exchange through the warp's padded buffer, Z = c-Z_j).
+// Two 32-double planes per thread (168 registers): 12 warps (6 pairs, 12 circuits in flight per
+// SM), one exchange buffer per warp (the segments use it in turn, guarded by __syncwarp).
+#pragma once
+
+#include "plane.cuh"
+
+namespace dvqls {
+namespace plane2 {
+
+using plane::BATCH;
+using plane::BUF;
+using plane::lds_a;
+using plane::N;
+using plane::NQ;
+using plane::R;
+using plane::RB;
+using plane::ROW;
+using plane::sts_a;
+using plane::TB;
+using plane::XALIGN;
+using plane::XREG;
+
+constexpr int WARPS = 12;
+constexpr int NP = WARPS / 2;
+
+template <int B0, int B1>
+__device__ __forceinline__ void fwht(double (&v)[R]) { plane::fwht<B0, B1>(v); }
+
+// a4: phi_i = sgn_k(i ^ m_k) x_pl[i ^ m_k] in layout A (sign and plane are address bits)
+__device__ __forceinline__ void gather(double (&v)[R], uint32_t xa, uint32_t pl, uint32_t t, const PauliTerm& Tk) {
+  const uint32_t mh = Tk.xm >> TB, tl = t ^ (Tk.xm & 31u), zh = Tk.zm >> TB;
+  const uint32_t sg0 = (__popc(tl & Tk.zm & 31u) ^ __popc(mh & zh)) & 1u;
+  uint32_t a = (xa + (pl << (NQ + 4))) | (((sg0 << NQ) | (mh << TB) | tl) * 8u);
+#pragma unroll
+  for (int kk = 0; kk < R; ++kk) {
+    const int r = kk ^ (kk >> 1);
+    if (kk) {
+      const int bb = ctz_c(kk);
+      a ^= ((1u << (TB + bb)) | (((zh >> bb) & 1u) << NQ)) * 8u;
+    }
+    v[r] = lds_a(a);
+  }
+}
+
+__device__ __forceinline__ void store_A(const double (&v)[R], uint32_t baseA) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) sts_a(baseA + uint32_t(r) * ROW, v[r]);
+}
+__device__ __forceinline__ void store_B(const double (&v)[R], uint32_t baseB) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) sts_a(baseB + uint32_t(r) * 8u, v[r]);
+}
+__device__ __forceinline__ void load_A(double (&v)[R], uint32_t baseA) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = lds_a(baseA + uint32_t(r) * ROW);
+}
+__device__ __forceinline__ void load_B(double (&v)[R], uint32_t baseB) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = lds_a(baseB + uint32_t(r) * 8u);
+}
+
+// a6: c-Z_j in layout B (register bit p, or lane bit p - 5)
+__device__ __forceinline__ void zflip(double (&v)[R], int p, uint32_t t) {
+  if (p < RB) {
+#pragma unroll
+    for (int bb = 0; bb < RB; ++bb)
+      if (bb == p) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (r & (1 << bb)) v[r] = flip(v[r], 0x80000000u);
+      }
+  } else {
+    const uint32_t m = uint32_t((t >> (p - RB)) & 1) << 31;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = flip(v[r], m);
+  }
+}
+
+// a8: this plane's half of Re(i^q S), S = sum_j conj(x'_j) phi_j (plane.cuh), warp-summed
+__device__ __forceinline__ double readout(const double (&v)[R], uint32_t xa, uint32_t pl, uint32_t t,
+                                          const PauliTerm& Tl, int q) {
+  const uint32_t qi = uint32_t(q & 1);
+  const uint32_t rp = pl ^ qi, xs = qi & (pl ^ 1u);
+  const uint32_t mh = Tl.xm >> TB, tl = t ^ (Tl.xm & 31u), zh = Tl.zm >> TB;
+  const uint32_t sg0 = (__popc(t & Tl.zm & 31u) & 1u) ^ xs;
+  uint32_t a = (xa + (rp << (NQ + 4))) | (((sg0 << NQ) | (mh << TB) | tl) * 8u);
+  double ac[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int kk = 0; kk < R; ++kk) {
+    const int r = kk ^ (kk >> 1);
+    if (kk) {
+      const int bb = ctz_c(kk);
+      a ^= ((1u << (TB + bb)) | (((zh >> bb) & 1u) << NQ)) * 8u;
+    }
+    ac[kk & 3] = fma(lds_a(a), v[r], ac[kk & 3]);
+  }
+  double half = (ac[0] + ac[1]) + (ac[2] + ac[3]);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) half += __shfl_xor_sync(0xffffffffu, half, off);
+  return half;
+}
+
+struct Dec {  // canonical decode of a circuit, advanced without divisions
+  int part, s, k, l;
+  __device__ __forceinline__ void next(int n1, int L) {
+    if (++part == 2) {
+      part = 0;
+      if (++s == n1) {
+        s = 0;
+        if (++k == L) { k = 0; ++l; }
+      }
+    }
+  }
+};
+
+template <int W>
+__host__ __device__ constexpr size_t small_bytes() {
+  return sizeof(double) * (size_t(W / 2) * 2 * BATCH * 2 + size_t(W / 2) * 4);
+}
+
+__global__ void __launch_bounds__(WARPS * 32, 1)  // <= 168 registers: 12 warps per SM
+plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ tab, const double2* __restrict__ coef,
+              const double2* __restrict__ hv, double hv_scale, int L, int64_t c0, int64_t C, int K,
+              double* __restrict__ out_terms, double* __restrict__ partials, int with_cost,
+              double* __restrict__ red_out, unsigned* __restrict__ counter, P2PArgs p2p) {
+  pdl_wait();
+  (void)hv; (void)hv_scale;
+  constexpr size_t SMALL = small_bytes<WARPS>();
+  double* sslot = reinterpret_cast<double*>(dvqls_smem);
+  double* sacc = sslot + NP * 2 * BATCH * 2;
+  const uint32_t sb = plane::sbase();
+  const uint32_t xa = (sb + uint32_t(SMALL) + XALIGN - 1) & ~(XALIGN - 1);
+  {
+    uint32_t dsz;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsz));
+    if (xa + XREG + WARPS * BUF - sb > dsz) __trap();
+  }
+  double* sd = reinterpret_cast<double*>(reinterpret_cast<char*>(dvqls_smem) + (xa - sb));
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t t = threadIdx.x & 31;
+  const int pair = warp >> 1;
+  const uint32_t pl = uint32_t(warp & 1);
+  const uint32_t buf = xa + XREG + uint32_t(warp) * BUF;
+  const uint32_t baseA = buf + t * 8u, baseB = buf + t * ROW;
+  const int n1 = NQ + 1;
+  double* slot = sslot + pair * (2 * BATCH * 2);
+  double* pacc = sacc + 4 * pair;
+
+  const int64_t G = gridDim.x;
+  const int64_t w0 = wcum(c0, NQ), Wt = wcum(c0 + C, NQ) - w0, Wall = Wt * K;
+  auto flat_of = [&](int64_t w) -> int64_t {
+    if (w >= Wall) return int64_t(K) * C;
+    const int64_t th = w / Wt, rem = w - th * Wt;
+    const int64_t c = min(max(winv(w0 + rem, NQ) - c0, int64_t(0)), C);
+    return th * C + c;
+  };
+  const int64_t Fb = Wall > 0 ? flat_of(Wall * (int64_t)blockIdx.x / G) : 0;
+  const int64_t Fe =
+      Wall <= 0 ? 0 : blockIdx.x + 1 == G ? int64_t(K) * C : flat_of(Wall * ((int64_t)blockIdx.x + 1) / G);
+  const int th_first = C > 0 ? int(Fb / C) : 0, th_last = Fe > Fb ? int((Fe - 1) / C) : th_first - 1;
+  for (int k = threadIdx.x; k < K; k += blockDim.x)
+    if (k < th_first || k > th_last)
+      for (int q = 0; q < 4; ++q) partials[(size_t(k) * G + blockIdx.x) * 4 + q] = 0.0;
+
+  for (int kth = th_first; kth <= th_last; ++kth) {
+    const int64_t pa = max(Fb, int64_t(kth) * C) - int64_t(kth) * C;
+    const int64_t pb = min(Fe, int64_t(kth + 1) * C) - int64_t(kth) * C;
+    const double2* x = x_all + (size_t)kth * N;
+    __syncthreads();
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const double2 a = x[i];
+      sd[i] = a.x;
+      sd[N + i] = -a.x;
+      sd[2 * N + i] = a.y;
+      sd[3 * N + i] = -a.y;
+    }
+    __syncthreads();
+    int cb, ce;
+    {
+      int64_t b, e;
+      weighted_range(c0 + pa, pb - pa, pair, NP, NQ, &b, &e);
+      cb = int(pa + b);
+      ce = int(pa + e);
+    }
+    if (pl == 0 && t == 0) pacc[0] = pacc[1] = pacc[2] = pacc[3] = 0.0;
+    Dec d;
+    {
+      const int64_t c = c0 + cb, tk = c >> 1, lk = tk / n1;
+      d.part = int(c & 1);
+      d.s = int(tk % n1);
+      d.k = int(lk % L);
+      d.l = int(lk / L);
+    }
+
+    // a9 (fused): pair combine every BATCH circuits (plane.cuh)
+    auto deposit = [&](int cl, double half) {
+      const int j = (cl - cb) & (BATCH - 1);
+      double* sl = slot + (((cl - cb) / BATCH) & 1) * (BATCH * 2);
+      if (t == 0) sl[2 * j + pl] = half;
+      if (j == BATCH - 1 || cl + 1 == ce) {
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + pair), "r"(64) : "memory");
+        if (pl == 0) {
+          double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+          if (int(t) <= j) {
+            const double val = sl[2 * t] + sl[2 * t + 1];
+            const int cc = cl - j + int(t);
+            out_terms[(size_t)kth * C + cc] = val;
+            const int64_t c = c0 + cc, tk = c >> 1, lk = tk / n1;
+            const int prt = int(c & 1), ss = int(tk - lk * n1), kk = int(lk % L), ll = int(lk / L);
+            const double2 cl_ = coef[ll], ck = coef[kk];
+            const double wr = cl_.x * ck.x + cl_.y * ck.y, wi = cl_.x * ck.y - cl_.y * ck.x;
+            const double cr = (prt == 0 ? wr : -wi) * val, ci = (prt == 0 ? wi : wr) * val;
+            if (ss == 0) { e2 = cr; e3 = ci; } else { e0 = cr; e1 = ci; }
+          }
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) {
+            e0 += __shfl_xor_sync(0xffffffffu, e0, off);
+            e1 += __shfl_xor_sync(0xffffffffu, e1, off);
+            e2 += __shfl_xor_sync(0xffffffffu, e2, off);
+            e3 += __shfl_xor_sync(0xffffffffu, e3, off);
+          }
+          if (t == 0) { pacc[0] += e0; pacc[1] += e1; pacc[2] += e2; pacc[3] += e3; }
+        }
+      }
+    };
+    // one circuit on its own (range ends, denominators)
+    auto single = [&](int cl, const Dec& dd) {
+      const PauliTerm Tk = tab[dd.k];
+      double v[R];
+      gather(v, xa, pl, t, Tk);
+      double scale = 1.0;
+      if (dd.s > 0) {
+        fwht<0, RB>(v);
+        plane::exchange<true>(v, baseA, baseB);
+        fwht<0, TB>(v);
+        zflip(v, NQ - dd.s, t);
+        fwht<0, TB>(v);
+        plane::exchange<false>(v, baseA, baseB);
+        fwht<0, RB>(v);
+        scale = 1.0 / double(N);
+      }
+      const PauliTerm Tl = tab[dd.l];
+      const int q = (Tk.ny + Tl.ny + 3 * dd.part) & 3;
+      double half = readout(v, xa, pl, t, Tl, q);
+      half *= (q == 1 || q == 2) ? -scale : scale;
+      deposit(cl, half);
+    };
+
+    int cl = cb;
+    if (cl < ce && ((c0 + cl) & 1)) {  // pairs start on a Re circuit: (Re, Im) of one task
+      single(cl, d);
+      d.next(n1, L);
+      ++cl;
+    }
+    for (; cl + 1 < ce; cl += 2) {
+      const Dec da = d;
+      d.next(n1, L);
+      const Dec db = d;
+      d.next(n1, L);
+      if (da.s == 0) {  // denominator pair: gather + readout each
+        single(cl, da);
+        single(cl + 1, db);
+        continue;
+      }
+      // numerator pair (Re, Im circuits of one task: same k, l, s), skewed by one phase
+      const PauliTerm Tk = tab[da.k];
+      const int p = NQ - da.s;
+      double va[R], vb[R];
+      gather(va, xa, pl, t, Tk);
+      // seg 1: F1(A) | gather(B)
+      fwht<0, RB>(va);
+      gather(vb, xa, pl, t, Tk);
+      // seg 2: X1(A) | F1(B)
+      __syncwarp();
+      store_A(va, baseA);
+      fwht<0, 3>(vb);
+      __syncwarp();
+      load_B(va, baseB);
+      fwht<3, RB>(vb);
+      // seg 3: F2 Z F3 (A) | X1(B)
+      __syncwarp();
+      store_A(vb, baseA);
+      fwht<0, TB>(va);
+      zflip(va, p, t);
+      __syncwarp();
+      load_B(vb, baseB);
+      fwht<0, TB>(va);
+      // seg 4: X2(A) | F2 Z F3 (B)
+      __syncwarp();
+      store_B(va, baseB);
+      fwht<0, TB>(vb);
+      zflip(vb, p, t);
+      __syncwarp();
+      load_A(va, baseA);
+      fwht<0, TB>(vb);
+      // seg 5: F4(A) | X2(B)
+      __syncwarp();
+      store_B(vb, baseB);
+      fwht<0, 3>(va);
+      __syncwarp();
+      load_A(vb, baseA);
+      fwht<3, RB>(va);
+      // seg 6: readout(A) | F4(B);  seg 7: readout(B)
+      const PauliTerm Tl = tab[da.l];
+      const int qa = (Tk.ny + Tl.ny) & 3, qb = (Tk.ny + Tl.ny + 3) & 3;
+      double ha = readout(va, xa, pl, t, Tl, qa);
+      fwht<0, RB>(vb);
+      double hb = readout(vb, xa, pl, t, Tl, qb);
+      constexpr double sc = 1.0 / double(N);
+      ha *= (qa == 1 || qa == 2) ? -sc : sc;
+      hb *= (qb == 1 || qb == 2) ? -sc : sc;
+      deposit(cl, ha);
+      deposit(cl + 1, hb);
+    }
+    if (cl < ce) {
+      single(cl, d);
+      d.next(n1, L);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // fixed pair order
+      double e0 = 0, e1 = 0, e2 = 0, e3 = 0;
+      for (int g = 0; g < NP; ++g) {
+        e0 += sacc[4 * g]; e1 += sacc[4 * g + 1]; e2 += sacc[4 * g + 2]; e3 += sacc[4 * g + 3];
+      }
+      double* o = partials + ((size_t)kth * G + blockIdx.x) * 4;
+      o[0] = e0; o[1] = e1; o[2] = e2; o[3] = e3;
+    }
+  }
+  if (red_out) finish_all(partials, int(G), K, NQ, with_cost, red_out, counter, p2p);
+}
+
+// dynamic SMEM to request when the dynamic base sits at shared-window address sb
+__host__ __device__ constexpr size_t smem_bytes(uint32_t sb) {
+  return ((sb + small_bytes<WARPS>() + XALIGN - 1) & ~size_t(XALIGN - 1)) - sb + XREG + size_t(WARPS) * BUF;
+}
+
+}  // namespace plane2
+}  // namespace dvqls

@@ -31,10 +31,11 @@ def dv():
     return dvqls
 
 
+@pytest.mark.parametrize("variant", [1, 2])
 @pytest.mark.parametrize("L,seed", [(3, 1), (5, 2), (7, 3)])
-def test_random_lcu_n10(dv, L, seed):
+def test_random_lcu_n10(dv, L, seed, variant):
     w = configs.random_workload(10, L, 2, seed=200 + seed)
-    ctx = dv.from_workload(w)
+    ctx = dv.from_workload(w, variant=variant)
     try:
         th = w.theta0()
         g = ctx.terms(th)
@@ -47,10 +48,11 @@ def test_random_lcu_n10(dv, L, seed):
         ctx.destroy()
 
 
-def test_theta_batch_n10(dv):
+@pytest.mark.parametrize("variant", [1, 2])
+def test_theta_batch_n10(dv, variant):
     """K thetas in one flattened grid: every cost equals the oracle's for its theta."""
     w = configs.random_workload(10, 4, 2, seed=211)
-    ctx = dv.from_workload(w)
+    ctx = dv.from_workload(w, variant=variant)
     try:
         ths = np.stack([w.theta0(s) for s in range(6)])
         cb, _ = ctx.cost_batch(ths)
@@ -88,3 +90,24 @@ def test_cfg3_launch_variants_bitwise(dv):
     finally:
         for ctx in ctxs:
             ctx.destroy()
+
+
+def test_cfg3_two_circuits_per_warp_matches_one(dv):
+    """plane2_kernel (two circuits in flight per warp, skewed phases) computes every circuit with
+    the same operations in the same order as plane_kernel: bitwise identical terms at cfg3; the
+    weighted sums differ only in summation grouping (6 vs 10 warp pairs per CTA)."""
+    w = configs.cfg3()
+    th = w.theta0(7)
+    a = dv.from_workload(w, variant=1)
+    b = dv.from_workload(w, variant=2)
+    try:
+        ta, tb = a.terms(th), b.terms(th)
+        ca, cb = a.cost(th), b.cost(th)
+        ths = np.stack([w.theta0(s) for s in range(16)])
+        ba, bb = a.cost_batch(ths)[0], b.cost_batch(ths)[0]
+    finally:
+        a.destroy()
+        b.destroy()
+    assert np.array_equal(ta, tb)
+    assert abs(ca - cb) <= 1e-13 and np.max(np.abs(ba - bb)) <= 1e-13
+    assert np.max(np.abs(ta - sim.workload_terms(w, th))) <= TOL
