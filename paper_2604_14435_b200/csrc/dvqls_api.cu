@@ -281,7 +281,22 @@ int launch_prefix(dvqls_ctx* ctx, int K, const double* thetas_dev) {
     if (e) return fail(ctx, DVQLS_E_CUDA, "global prefix: %s", cudaGetErrorString(cudaError_t(e)));
     return DVQLS_OK;
   }
-  if (ctx->pc.with_n) {
+  if (ctx->pc.cluster > 0) {  // thread-block cluster of pc.cluster CTAs per theta (prefix_cluster.cuh)
+    void* args[] = {(void*)&ctx->layers, (void*)&ctx->entangler, (void*)&thetas_dev, (void*)&ctx->d_x};
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(ctx->pc.cluster, K);
+    lc.blockDim = dim3(ctx->pc.threads);
+    lc.dynamicSmemBytes = ctx->pc.smem;
+    lc.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ctx->pc.cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelExC(&lc, ctx->pc.fn, args));
+  } else if (ctx->pc.with_n) {
     void* args[] = {(void*)&ctx->n, (void*)&ctx->layers, (void*)&ctx->entangler, (void*)&thetas_dev,
                     (void*)&ctx->d_x};
     CK(cudaLaunchKernel(ctx->pc.fn, dim3(K), dim3(ctx->pc.threads), args, ctx->pc.smem, ctx->stream));
@@ -553,6 +568,10 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
     fail(ctx, DVQLS_E_ARG, "entangler must be 0 (CNOT ring) or 1 (CZ ring)");
     return bail(DVQLS_E_ARG);
   }
+  if (o.prefix < 0 || o.prefix > 1) {
+    fail(ctx, DVQLS_E_ARG, "prefix must be 0 or 1");
+    return bail(DVQLS_E_ARG);
+  }
   if (o.variant < 0 || o.variant > 2) {
     fail(ctx, DVQLS_E_ARG, "variant must be 0, 1 or 2");
     return bail(DVQLS_E_ARG);
@@ -770,7 +789,7 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
 
   // ---- prefix (a2) ----------------------------------------------------------------------
   if (n <= 12) {
-    ctx->pc = prefix_cfg(n, layers);
+    ctx->pc = prefix_cfg(n, layers, o.prefix != 1);
     if (!ctx->pc.fn || cudaFuncSetAttribute(ctx->pc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             int(ctx->pc.smem)) != cudaSuccess) {
       fail(ctx, DVQLS_E_CUDA, "prefix kernel smem %zu B", ctx->pc.smem);

@@ -7,6 +7,7 @@
 #include "launch.h"
 #include "plane.cuh"
 #include "plane2.cuh"
+#include "prefix_cluster.cuh"
 
 namespace dvqls {
 
@@ -44,7 +45,7 @@ KernelCfg plane2_cfg() {
   return k;
 }
 
-PrefixCfg prefix_cfg(int n, int layers) {
+PrefixCfg prefix_cfg(int n, int layers, bool cluster) {
   static const void* quads[11] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                                   (const void*)&prefix_quad_kernel<7>, (const void*)&prefix_quad_kernel<8>,
                                   (const void*)&prefix_quad_kernel<9>, (const void*)&prefix_quad_kernel<10>};
@@ -52,8 +53,27 @@ PrefixCfg prefix_cfg(int n, int layers) {
                                  (const void*)&prefix_lanes_kernel<1>, (const void*)&prefix_lanes_kernel<2>,
                                  (const void*)&prefix_lanes_kernel<3>, (const void*)&prefix_lanes_kernel<4>,
                                  (const void*)&prefix_lanes_kernel<5>, (const void*)&prefix_lanes_kernel<6>};
+  static const void* clus[11] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                 (const void*)&pclus::prefix_cluster_kernel<7>, (const void*)&pclus::prefix_cluster_kernel<8>,
+                                 (const void*)&pclus::prefix_cluster_kernel<9>, (const void*)&pclus::prefix_cluster_kernel<10>};
+  static const size_t csm[11] = {0, 0, 0, 0, 0, 0, 0, sizeof(double2) * pclus::smem_doubles2<7>(1),
+                                 sizeof(double2) * pclus::smem_doubles2<8>(1), sizeof(double2) * pclus::smem_doubles2<9>(1),
+                                 sizeof(double2) * pclus::smem_doubles2<10>(1)};
   PrefixCfg p;
   const size_t N = size_t(1) << n;
+  // 7 <= n <= 10: the state spread over a cluster of 2^(n-7) CTAs joined by DSMEM (one amplitude per
+  // thread), while its tables fit the SMEM of one CTA (they grow with the depth)
+  if (cluster && n >= 7 && n <= 10) {
+    const size_t per_layer = csm[n] - sizeof(double2) * 3 * pclus::NL;
+    const size_t bytes = sizeof(double2) * 3 * pclus::NL + per_layer * size_t(layers);
+    if (bytes <= size_t(200) << 10) {
+      p.fn = clus[n];
+      p.threads = pclus::NL;
+      p.smem = bytes;
+      p.cluster = 1 << (n - pclus::LB);
+      return p;
+    }
+  }
   if (n >= 7 && n <= 10) {  // 4 amplitudes per thread, shuffles + 2 transposes per layer
     p.fn = quads[n];
     p.threads = std::max(32, int(N / 4));

@@ -244,98 +244,83 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
         }
       }
     };
-    // one circuit on its own (range ends, denominators)
-    auto single = [&](int cl, const Dec& dd) {
-      const PauliTerm Tk = tab[dd.k];
-      double v[R];
-      gather(v, xa, pl, t, Tk);
-      double scale = 1.0;
-      if (dd.s > 0) {
-        fwht<0, RB>(v);
-        plane::exchange<true>(v, baseA, baseB);
-        fwht<0, TB>(v);
-        zflip(v, NQ - dd.s, t);
-        fwht<0, TB>(v);
-        plane::exchange<false>(v, baseA, baseB);
-        fwht<0, RB>(v);
-        scale = 1.0 / double(N);
-      }
-      const PauliTerm Tl = tab[dd.l];
-      const int q = (Tk.ny + Tl.ny + 3 * dd.part) & 3;
-      double half = readout(v, xa, pl, t, Tl, q);
-      half *= (q == 1 || q == 2) ? -scale : scale;
-      deposit(cl, half);
-    };
-
-    int cl = cb;
-    if (cl < ce && ((c0 + cl) & 1)) {  // pairs start on a Re circuit: (Re, Im) of one task
-      single(cl, d);
-      d.next(n1, L);
-      ++cl;
-    }
-    for (; cl + 1 < ce; cl += 2) {
+    // one loop, one copy of each path (instruction-cache footprint): a unit is either a numerator
+    // pair (the Re and Im circuits of one task, skewed) or a single circuit (denominators, range ends)
+#pragma unroll 1
+    for (int cl = cb; cl < ce;) {
       const Dec da = d;
       d.next(n1, L);
-      const Dec db = d;
-      d.next(n1, L);
-      if (da.s == 0) {  // denominator pair: gather + readout each
-        single(cl, da);
-        single(cl + 1, db);
-        continue;
-      }
-      // numerator pair (Re, Im circuits of one task: same k, l, s), skewed by one phase
       const PauliTerm Tk = tab[da.k];
-      const int p = NQ - da.s;
-      double va[R], vb[R];
-      gather(va, xa, pl, t, Tk);
-      // seg 1: F1(A) | gather(B)
-      fwht<0, RB>(va);
-      gather(vb, xa, pl, t, Tk);
-      // seg 2: X1(A) | F1(B)
-      __syncwarp();
-      store_A(va, baseA);
-      fwht<0, 3>(vb);
-      __syncwarp();
-      load_B(va, baseB);
-      fwht<3, RB>(vb);
-      // seg 3: F2 Z F3 (A) | X1(B)
-      __syncwarp();
-      store_A(vb, baseA);
-      fwht<0, TB>(va);
-      zflip(va, p, t);
-      __syncwarp();
-      load_B(vb, baseB);
-      fwht<0, TB>(va);
-      // seg 4: X2(A) | F2 Z F3 (B)
-      __syncwarp();
-      store_B(va, baseB);
-      fwht<0, TB>(vb);
-      zflip(vb, p, t);
-      __syncwarp();
-      load_A(va, baseA);
-      fwht<0, TB>(vb);
-      // seg 5: F4(A) | X2(B)
-      __syncwarp();
-      store_B(vb, baseB);
-      fwht<0, 3>(va);
-      __syncwarp();
-      load_A(vb, baseA);
-      fwht<3, RB>(va);
-      // seg 6: readout(A) | F4(B);  seg 7: readout(B)
       const PauliTerm Tl = tab[da.l];
-      const int qa = (Tk.ny + Tl.ny) & 3, qb = (Tk.ny + Tl.ny + 3) & 3;
-      double ha = readout(va, xa, pl, t, Tl, qa);
-      fwht<0, RB>(vb);
-      double hb = readout(vb, xa, pl, t, Tl, qb);
-      constexpr double sc = 1.0 / double(N);
-      ha *= (qa == 1 || qa == 2) ? -sc : sc;
-      hb *= (qb == 1 || qb == 2) ? -sc : sc;
-      deposit(cl, ha);
-      deposit(cl + 1, hb);
-    }
-    if (cl < ce) {
-      single(cl, d);
-      d.next(n1, L);
+      if (da.s > 0 && da.part == 0 && cl + 1 < ce) {
+        d.next(n1, L);  // the Im circuit of the same task
+        const int p = NQ - da.s;
+        double va[R], vb[R];
+        gather(va, xa, pl, t, Tk);
+        // seg 1: F1(A) | gather(B)
+        fwht<0, RB>(va);
+        gather(vb, xa, pl, t, Tk);
+        // seg 2: X1(A) | F1(B)
+        __syncwarp();
+        store_A(va, baseA);
+        fwht<0, 3>(vb);
+        __syncwarp();
+        load_B(va, baseB);
+        fwht<3, RB>(vb);
+        // seg 3: F2 Z F3 (A) | X1(B)
+        __syncwarp();
+        store_A(vb, baseA);
+        fwht<0, TB>(va);
+        zflip(va, p, t);
+        __syncwarp();
+        load_B(vb, baseB);
+        fwht<0, TB>(va);
+        // seg 4: X2(A) | F2 Z F3 (B)
+        __syncwarp();
+        store_B(va, baseB);
+        fwht<0, TB>(vb);
+        zflip(vb, p, t);
+        __syncwarp();
+        load_A(va, baseA);
+        fwht<0, TB>(vb);
+        // seg 5: F4(A) | X2(B)
+        __syncwarp();
+        store_B(vb, baseB);
+        fwht<0, 3>(va);
+        __syncwarp();
+        load_A(vb, baseA);
+        fwht<3, RB>(va);
+        // seg 6: readout(A) | F4(B);  seg 7: readout(B)
+        const int qa = (Tk.ny + Tl.ny) & 3, qb = (Tk.ny + Tl.ny + 3) & 3;
+        double ha = readout(va, xa, pl, t, Tl, qa);
+        fwht<0, RB>(vb);
+        double hb = readout(vb, xa, pl, t, Tl, qb);
+        constexpr double sc = 1.0 / double(N);
+        ha *= (qa == 1 || qa == 2) ? -sc : sc;
+        hb *= (qb == 1 || qb == 2) ? -sc : sc;
+        deposit(cl, ha);
+        deposit(cl + 1, hb);
+        cl += 2;
+      } else {
+        double v[R];
+        gather(v, xa, pl, t, Tk);
+        double scale = 1.0;
+        if (da.s > 0) {
+          fwht<0, RB>(v);
+          plane::exchange<true>(v, baseA, baseB);
+          fwht<0, TB>(v);
+          zflip(v, NQ - da.s, t);
+          fwht<0, TB>(v);
+          plane::exchange<false>(v, baseA, baseB);
+          fwht<0, RB>(v);
+          scale = 1.0 / double(N);
+        }
+        const int q = (Tk.ny + Tl.ny + 3 * da.part) & 3;
+        double half = readout(v, xa, pl, t, Tl, q);
+        half *= (q == 1 || q == 2) ? -scale : scale;
+        deposit(cl, half);
+        cl += 1;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {  // fixed pair order

@@ -67,12 +67,13 @@ class _Opts(ctypes.Structure):
                 ("virtual_rank", ctypes.c_int), ("virtual_world", ctypes.c_int), ("allreduce", ctypes.c_int),
                 ("p2p_timeout_ms", ctypes.c_int), ("host_allgather", HOST_ALLGATHER),
                 ("host_allgather_user", ctypes.c_void_p), ("graphs", ctypes.c_int), ("pdl", ctypes.c_int),
-                ("stage", ctypes.c_int), ("stream_grid", ctypes.c_int), ("variant", ctypes.c_int)]
+                ("stage", ctypes.c_int), ("stream_grid", ctypes.c_int), ("variant", ctypes.c_int),
+                ("prefix", ctypes.c_int)]
 
 
 def _opts(device=-1, rank=0, world=1, nccl_id=None, entangler=0, stream=None, timing=False, max_batch=16, mode=0,
           workspace=(None, 0), virtual_rank=0, virtual_world=0, allreduce=DVQLS_ALLREDUCE_P2P, p2p_timeout_ms=0,
-          host_allgather=None, graphs=True, pdl=True, stage=0, stream_grid=0, variant=0):
+          host_allgather=None, graphs=True, pdl=True, stage=0, stream_grid=0, variant=0, prefix=0):
     op = _Opts()
     op.device, op.rank, op.world = int(device), int(rank), int(world)
     op.nccl_unique_id = nccl_id
@@ -85,7 +86,7 @@ def _opts(device=-1, rank=0, world=1, nccl_id=None, entangler=0, stream=None, ti
         op.host_allgather = host_allgather
     op.graphs = 0 if graphs else -1
     op.pdl = 0 if pdl else -1
-    op.stage, op.stream_grid, op.variant = int(stage), int(stream_grid), int(variant)
+    op.stage, op.stream_grid, op.variant, op.prefix = int(stage), int(stream_grid), int(variant), int(prefix)
     return op
 
 
@@ -217,7 +218,7 @@ class Context:
         least workspace_size(...) bytes, 256-byte aligned (dvqls_opts.workspace_dev).
         extra: the remaining dvqls_opts fields by name (virtual_rank, virtual_world, allreduce,
         p2p_timeout_ms, host_allgather (a HOST_ALLGATHER, see make_host_allgather), graphs, pdl,
-        stage, stream_grid, variant)."""
+        stage, stream_grid, variant, prefix)."""
         L = load()
         self.n, self.layers = int(n), int(layers)
         self.P = 3 * self.n * self.layers
