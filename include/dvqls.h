@@ -129,8 +129,9 @@ typedef struct dvqls_opts {
   int variant;                 /* kernel variant for n = 10, uniform b: 0 = default, 1 = one circuit
                                   per warp (plane_kernel), 2 = two circuits in flight per warp
                                   (plane2_kernel).  Same circuits and results to rounding.     */
-  int prefix;                  /* V(theta)|0> for 7 <= n <= 10: 0 = on a thread-block cluster of
-                                  2^(n-7) CTAs joined by DSMEM (default); 1 = one CTA per theta */
+  int prefix;                  /* V(theta)|0> for 7 <= n <= 10: 0 = one CTA per theta (default);
+                                  1 = a thread-block cluster of 2^(n-7) CTAs per theta joined by
+                                  DSMEM (measured no faster on B200: DESIGN.md §6)              */
 } dvqls_opts;
 
 #define DVQLS_ALLREDUCE_P2P 0

@@ -789,7 +789,7 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
 
   // ---- prefix (a2) ----------------------------------------------------------------------
   if (n <= 12) {
-    ctx->pc = prefix_cfg(n, layers, o.prefix != 1);
+    ctx->pc = prefix_cfg(n, layers, o.prefix == 1);
     if (!ctx->pc.fn || cudaFuncSetAttribute(ctx->pc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             int(ctx->pc.smem)) != cudaSuccess) {
       fail(ctx, DVQLS_E_CUDA, "prefix kernel smem %zu B", ctx->pc.smem);

@@ -61,8 +61,11 @@ PrefixCfg prefix_cfg(int n, int layers, bool cluster) {
                                  sizeof(double2) * pclus::smem_doubles2<10>(1)};
   PrefixCfg p;
   const size_t N = size_t(1) << n;
-  // 7 <= n <= 10: the state spread over a cluster of 2^(n-7) CTAs joined by DSMEM (one amplitude per
-  // thread), while its tables fit the SMEM of one CTA (they grow with the depth)
+  // cluster: 7 <= n <= 10, the state spread over 2^(n-7) CTAs joined by DSMEM (one amplitude per
+  // thread), while its tables fit the SMEM of one CTA (they grow with the depth).  Measured at cfg3
+  // (profiles/r2_cluster_prefix/): 20-24 us vs 21-23 us for the one-CTA kernel -- the per-layer
+  // cluster barrier (~0.9 K cycles with skew) and the 8x-redundant DSMEM gather (~1-1.6 K cycles)
+  // cost what the 8 SMs save -- so it is the opt-in variant (opts.prefix = 1).
   if (cluster && n >= 7 && n <= 10) {
     const size_t per_layer = csm[n] - sizeof(double2) * 3 * pclus::NL;
     const size_t bytes = sizeof(double2) * 3 * pclus::NL + per_layer * size_t(layers);

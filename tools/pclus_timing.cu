@@ -1,83 +1,16 @@
-// prefix_cluster.cuh - a2 for 7 <= n <= 10 on a thread-block CLUSTER: x = V(theta)|0^n> spread
-// over CS = 2^(n-7) CTAs whose shared memories are joined through DSMEM (
-// SURVEY §8(c) readings 6-9).
-//
-// One theta's 2^n amplitudes used to live in ONE CTA (prefix_quad_kernel): a latency-bound
-// 20 us chain on a single SM that every cost call pays before any circuit can start (the K = 1
-// fixed cost).  Here the state is split over the cluster, one amplitude per thread:
-//   global index i = (rank << 7) | tid,  tid = (warp << 5) | lane,
-//   positions 0..4 = lane bits, 5..6 = warp bits, 7..n-1 = cluster bits (the CTA rank).
-// A layer (per qubit Ry Rz Ry fused into one SU(2) gate U_q, then the entangling ring) is
-//   1. lane-bit gates: one shuffle of the partner amplitude + a 2-term complex dot each;
-//   2. warp-bit gates (positions 5, 6) together: amplitudes through the CTA's SMEM, one barrier,
-//      new value = sum over the 4 partners of (U_5 (x) U_6)[row, col] * partner;
-//   3. cluster-bit gates (positions >= 7) AND the ring together: every CTA publishes its 128
-//      amplitudes, one cluster barrier, then thread i reads, from all CS CTAs over DSMEM, the
-//      amplitudes at local index j(p) of p = ring(i) and forms
-//          x'[i] = sign(i) * sum_c' (U_{7} (x) ... (x) U_{n-1})[c(p), c'] * S_c'[j(p)]
-//      (new[i] = old[ring(i)] for the CNOT ring, old[i] (-1)^{...} for the CZ ring).
-// The Kronecker tables of steps 2 and 3 are built once per call from the gate table.  One CTA
-// barrier and one cluster barrier per layer; the CS SMs share the FP64 work of the layer.
-// Exchange buffers are double-buffered by layer parity, so a CTA may publish layer l+1 while a
-// peer still reads layer l; a final cluster barrier keeps every CTA's SMEM alive until its peers
-// have read the last layer.
-#pragma once
-
-#include "kernels.cuh"
-
-namespace dvqls {
-namespace pclus {
-
-constexpr int LB = 7;          // local bits per CTA (lane 0..4, warp 5..6)
-constexpr int NL = 1 << LB;    // amplitudes (= threads) per CTA
-
-template <int NQ>
-struct PC {
-  static constexpr int CB = NQ - LB;  // cluster bits
-  static constexpr int CS = 1 << CB;  // CTAs per cluster
-};
-
-__device__ __forceinline__ uint32_t cta_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ double2 ld_dsmem(uint32_t addr) {
-  double2 v;
-  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
-  return v;
-}
-__device__ __forceinline__ void cluster_barrier() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
-__device__ __forceinline__ double2 cmac(double2 a, double2 b, double2 acc) {  // acc + a b
-  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
-}
-// entry (row, col) of U = [[a, -conj(b)], [b, conj(a)]] (gate table: a, b per gate)
-__device__ __forceinline__ double2 uent(const double2* U, int g, int row, int col) {
-  const double2 a = U[2 * g], b = U[2 * g + 1];
-  if (row == 0) return col == 0 ? a : make_double2(-b.x, b.y);
-  return col == 0 ? b : make_double2(a.x, -a.y);
-}
-
-// dynamic SMEM (double2 units): gates 2G | warp tables 16 per layer | cluster tables CS^2 per layer
-// | warp-bit exchange 128 | published amplitudes 2 x 128
-template <int NQ>
-__host__ __device__ constexpr size_t smem_doubles2(int layers) {
-  return size_t(2) * NQ * layers + size_t(16) * layers + size_t(PC<NQ>::CS) * PC<NQ>::CS * layers + 3 * NL;
-}
-
+// pclus_timing.cu - clock64 timestamps of the phases of the cluster prefix (prefix_cluster.cuh),
+// thread 0 of CTA 0, n = 10, d = 10: tables, then per layer lane gates / warp step / cluster barrier
+// / DSMEM gather.  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2604_14435_b200/csrc -o tools/pclus_timing tools/pclus_timing.cu
+#include <cstdio>
+#include <vector>
+#include "prefix_cluster.cuh"
+namespace dvqls { namespace pclus {
 template <int NQ>
 __global__ void __launch_bounds__(NL)
-prefix_cluster_kernel(int layers, int entangler, const double* __restrict__ thetas, double2* __restrict__ x_all) {
+prefix_cluster_timed(int layers, int entangler, const double* __restrict__ thetas, double2* __restrict__ x_all, long long* ts) {
+  int tsi = 0;
+#define TS_() do { if (threadIdx.x == 0 && blockIdx.x == 0) ts[tsi] = clock64(); ++tsi; } while (0)
+  TS_();
   pdl_trigger();
   constexpr int n = NQ, CB = PC<NQ>::CB, CS = PC<NQ>::CS;
   extern __shared__ double2 pcsm[];
@@ -138,6 +71,7 @@ prefix_cluster_kernel(int layers, int entangler, const double* __restrict__ thet
 #pragma unroll
   for (int c = 0; c < CS; ++c) remote[c] = (CS > 1 ? mapa(pub_base, uint32_t(c)) : pub_base) + pj * 16u;
   __syncthreads();  // tables ready
+  TS_();
 
   double2 v = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
   const unsigned full = 0xffffffffu;
@@ -152,6 +86,7 @@ prefix_cluster_kernel(int layers, int entangler, const double* __restrict__ thet
       const double2 pp = make_double2(__shfl_xor_sync(full, v.x, 1 << pos), __shfl_xor_sync(full, v.y, 1 << pos));
       v = cmac(co, pp, cmul(cs, v));
     }
+    TS_();
     // 2. warp bits (positions 5, 6): U_5 (x) U_6 over the 4 partners through SMEM
     sbuf[tid] = v;
     __syncthreads();
@@ -162,10 +97,12 @@ prefix_cluster_kernel(int layers, int entangler, const double* __restrict__ thet
       const double2 a1 = cmac(w[3], sbuf[(tid & 31) | (3 << 5)], cmul(w[2], sbuf[(tid & 31) | (2 << 5)]));
       v = make_double2(a0.x + a1.x, a0.y + a1.y);
     }
+    TS_();
     // 3. cluster bits + ring: publish, cluster barrier, gather over DSMEM
     const uint32_t par = uint32_t(layer & 1) * (NL * 16u);
     pub[(layer & 1) * NL + tid] = v;
     if (CS > 1) cluster_barrier(); else __syncthreads();
+    TS_();
     {
       const double2* gc = GC + CS * CS * layer + CS * pc;
       double2 r[CS];
@@ -180,10 +117,40 @@ prefix_cluster_kernel(int layers, int entangler, const double* __restrict__ thet
                                      (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y));
       v = neg ? make_double2(-s.x, -s.y) : s;
     }
+    TS_();
   }
   x_all[(size_t)blockIdx.y * (1u << n) + i] = v;
   if (CS > 1) cluster_barrier();  // peers may still read this CTA's last published layer
+  TS_();
 }
 
-}  // namespace pclus
-}  // namespace dvqls
+}}  // namespace dvqls::pclus
+using namespace dvqls::pclus;
+int main() {
+  const int n = 10, layers = 10, P = 3 * n * layers;
+  std::vector<double> th(P);
+  for (int i = 0; i < P; ++i) th[i] = 0.37 * i - 3.0;
+  double* dth; double2* dx; long long* dts;
+  cudaMalloc(&dth, P * 8); cudaMalloc(&dx, 16 << n); cudaMalloc(&dts, 4096 * 8);
+  cudaMemcpy(dth, th.data(), P * 8, cudaMemcpyHostToDevice);
+  const size_t smem = sizeof(double2) * (3 * NL) + (sizeof(double2) * smem_doubles2<10>(1) - sizeof(double2) * 3 * NL) * layers;
+  cudaFuncSetAttribute((const void*)&prefix_cluster_timed<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaLaunchConfig_t lc{}; lc.gridDim = dim3(8, 1); lc.blockDim = dim3(NL); lc.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension; at[0].val.clusterDim.x = 8;
+  at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1; lc.attrs = at; lc.numAttrs = 1;
+  int ent = 0;
+  void* args[] = {(void*)&layers, (void*)&ent, (void*)&dth, (void*)&dx, (void*)&dts};
+  for (int rep = 0; rep < 3; ++rep) cudaLaunchKernelExC(&lc, (const void*)&prefix_cluster_timed<10>, args);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int rep = 0; rep < 20; ++rep) cudaLaunchKernelExC(&lc, (const void*)&prefix_cluster_timed<10>, args);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  long long h[64]; cudaMemcpy(h, dts, sizeof h, cudaMemcpyDeviceToHost);
+  printf("{\"err\": \"%s\", \"us_per_launch_back_to_back\": %.2f, \"tables_cyc\": %lld", cudaGetErrorString(cudaGetLastError()), 1e3 * ms / 20, h[1] - h[0]);
+  long long s[4] = {0, 0, 0, 0};
+  for (int l = 0; l < layers; ++l) for (int q = 0; q < 4; ++q) s[q] += h[2 + 4 * l + q] - h[1 + 4 * l + q];
+  printf(", \"lane_cyc_per_layer\": %lld, \"warp_cyc_per_layer\": %lld, \"cbar_cyc_per_layer\": %lld, \"gather_cyc_per_layer\": %lld, \"final_cyc\": %lld, \"total_cyc\": %lld}\n",
+         s[0] / layers, s[1] / layers, s[2] / layers, s[3] / layers, h[2 + 4 * layers] - h[1 + 4 * layers], h[2 + 4 * layers] - h[0]);
+  return 0;
+}
