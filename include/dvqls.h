@@ -151,7 +151,7 @@ size_t dvqls_workspace_size(int n_qubits, int layers, int n_terms, const dvqls_o
  * (x_mask, z_mask, n_Y), copy coefficients, build U_b data, allocate device
  * buffers (the only cudaMalloc calls of the library; none when opts->workspace_dev
  * supplies the memory, see dvqls_workspace_size), pick this rank's
- * contiguous circuit block [c0, c1) = [rank*C/world, (rank+1)*C/world) of the
+ * contiguous block of whole tasks [c0, c1) (dvqls_shard_range) of the
  * C = 2(n+1)L^2 circuits ("strided workload allocation"; a contiguous
  * block balances equally) and, for world > 1, create the NCCL
  * communicator.  Collective over all ranks when world > 1.
@@ -301,9 +301,11 @@ int dvqls_launches_per_call(const dvqls_ctx* ctx);
  * on the context stream: ms[0] prefix, ms[1] Hadamard-test kernel, ms[2] reduction
  * (+ allreduce + finalize), ms[3] whole call.  Returns DVQLS_E_ARG if timing is off. */
 int dvqls_last_timings(const dvqls_ctx* ctx, float* ms4);
-/* Pure host helper (no device access): the contiguous circuit block
- * [c0, c1) = [floor(C*rank/world), floor(C*(rank+1)/world)) a rank evaluates.
- * Blocks of consecutive ranks tile [0, C) and differ in size by at most 1. */
+/* Pure host helper (no device access): the contiguous circuit block a rank evaluates, in whole
+ * tasks (the Re and Im circuits 2t, 2t+1 of a task stay together; P:394 allocates tasks):
+ *     [c0, c1) = [2 floor(T*rank/world), 2 floor(T*(rank+1)/world)),  T = floor(C/2),
+ * the last rank also taking circuit C-1 when C is odd.  Blocks of consecutive ranks tile [0, C)
+ * and differ in size by at most 2 (3 with an odd C). */
 int dvqls_shard_range(int64_t n_circuits, int rank, int world, int64_t* c0, int64_t* c1);
 /* Write a fresh 128-byte ncclUniqueId into out128 (rank 0 calls, then broadcasts). */
 int dvqls_nccl_unique_id(void* out128);

@@ -1275,8 +1275,9 @@ int dvqls_nccl_unique_id(void* out128) {
 
 int dvqls_shard_range(int64_t n_circuits, int rank, int world, int64_t* c0, int64_t* c1) {
   if (n_circuits < 0 || world < 1 || rank < 0 || rank >= world || !c0 || !c1) return DVQLS_E_ARG;
-  *c0 = n_circuits * rank / world;
-  *c1 = n_circuits * (rank + 1) / world;
+  const int64_t T = n_circuits / 2;  // whole tasks (Re, Im circuit pairs)
+  *c0 = 2 * (T * rank / world);
+  *c1 = rank + 1 == world ? n_circuits : 2 * (T * (rank + 1) / world);
   return DVQLS_OK;
 }
 

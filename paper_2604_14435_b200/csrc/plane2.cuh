@@ -79,21 +79,15 @@ __device__ __forceinline__ void load_B(double (&v)[R], uint32_t baseB) {
   for (int r = 0; r < R; ++r) v[r] = lds_a(baseB + uint32_t(r) * 8u);
 }
 
-// a6: c-Z_j in layout B (register bit p, or lane bit p - 5)
+// a6: c-Z_j in layout B (i = t << 5 | r: register bit p, or lane bit p - 5), branch-free: bit r of w
+// says whether register r flips, so the code after it is not duplicated per p
 __device__ __forceinline__ void zflip(double (&v)[R], int p, uint32_t t) {
-  if (p < RB) {
+  // column word of register bit p: 0xAAAAAAAA, 0xCCCCCCCC, 0xF0F0F0F0, 0xFF00FF00, 0xFFFF0000
+  const uint32_t cols = p == 0 ? 0xAAAAAAAAu : p == 1 ? 0xCCCCCCCCu : p == 2 ? 0xF0F0F0F0u : p == 3 ? 0xFF00FF00u
+                                                                                              : 0xFFFF0000u;
+  const uint32_t w = p < RB ? cols : (((t >> (p - RB)) & 1u) ? 0xFFFFFFFFu : 0u);
 #pragma unroll
-    for (int bb = 0; bb < RB; ++bb)
-      if (bb == p) {
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          if (r & (1 << bb)) v[r] = flip(v[r], 0x80000000u);
-      }
-  } else {
-    const uint32_t m = uint32_t((t >> (p - RB)) & 1) << 31;
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = flip(v[r], m);
-  }
+  for (int r = 0; r < R; ++r) v[r] = flip(v[r], (w << (31 - r)) & 0x80000000u);
 }
 
 // a8: this plane's half of Re(i^q S), S = sum_j conj(x'_j) phi_j (plane.cuh), warp-summed
@@ -169,12 +163,15 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
 
   const int64_t G = gridDim.x;
   const int64_t w0 = wcum(c0, NQ), Wt = wcum(c0 + C, NQ) - w0, Wall = Wt * K;
+  // every boundary on a task boundary (even circuit index; c0 and C are even, dvqls_shard_range), so
+  // a warp always holds the Re and Im circuits of one task together
   auto flat_of = [&](int64_t w) -> int64_t {
     if (w >= Wall) return int64_t(K) * C;
     const int64_t th = w / Wt, rem = w - th * Wt;
-    const int64_t c = min(max(winv(w0 + rem, NQ) - c0, int64_t(0)), C);
+    const int64_t c = min(max(winv(w0 + rem, NQ) - c0, int64_t(0)), C) & ~int64_t(1);
     return th * C + c;
   };
+  if ((c0 | C) & 1) __trap();  // host invariant: whole tasks per rank
   const int64_t Fb = Wall > 0 ? flat_of(Wall * (int64_t)blockIdx.x / G) : 0;
   const int64_t Fe =
       Wall <= 0 ? 0 : blockIdx.x + 1 == G ? int64_t(K) * C : flat_of(Wall * ((int64_t)blockIdx.x + 1) / G);
@@ -200,14 +197,14 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
     {
       int64_t b, e;
       weighted_range(c0 + pa, pb - pa, pair, NP, NQ, &b, &e);
-      cb = int(pa + b);
-      ce = int(pa + e);
+      cb = int(pa + (b & ~int64_t(1)));
+      ce = int(pa + (e & ~int64_t(1)));
     }
     if (pl == 0 && t == 0) pacc[0] = pacc[1] = pacc[2] = pacc[3] = 0.0;
     Dec d;
     {
       const int64_t c = c0 + cb, tk = c >> 1, lk = tk / n1;
-      d.part = int(c & 1);
+      d.part = 0;
       d.s = int(tk % n1);
       d.k = int(lk % L);
       d.l = int(lk / L);
@@ -244,16 +241,15 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
         }
       }
     };
-    // one loop, one copy of each path (instruction-cache footprint): a unit is either a numerator
-    // pair (the Re and Im circuits of one task, skewed) or a single circuit (denominators, range ends)
+    // one task (Re and Im circuit) per iteration; one copy of each path (instruction-cache footprint)
 #pragma unroll 1
-    for (int cl = cb; cl < ce;) {
+    for (int cl = cb; cl < ce; cl += 2) {
       const Dec da = d;
+      d.next(n1, L);
       d.next(n1, L);
       const PauliTerm Tk = tab[da.k];
       const PauliTerm Tl = tab[da.l];
-      if (da.s > 0 && da.part == 0 && cl + 1 < ce) {
-        d.next(n1, L);  // the Im circuit of the same task
+      if (da.s > 0) {  // numerator task: Re circuit A, Im circuit B, skewed by one phase
         const int p = NQ - da.s;
         double va[R], vb[R];
         gather(va, xa, pl, t, Tk);
@@ -300,26 +296,15 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
         hb *= (qb == 1 || qb == 2) ? -sc : sc;
         deposit(cl, ha);
         deposit(cl + 1, hb);
-        cl += 2;
-      } else {
-        double v[R];
-        gather(v, xa, pl, t, Tk);
-        double scale = 1.0;
-        if (da.s > 0) {
-          fwht<0, RB>(v);
-          plane::exchange<true>(v, baseA, baseB);
-          fwht<0, TB>(v);
-          zflip(v, NQ - da.s, t);
-          fwht<0, TB>(v);
-          plane::exchange<false>(v, baseA, baseB);
-          fwht<0, RB>(v);
-          scale = 1.0 / double(N);
+      } else {  // denominator task: c-A_k gather and c-A_l readout of each circuit
+#pragma unroll 1
+        for (int part = 0; part < 2; ++part) {
+          double v[R];
+          gather(v, xa, pl, t, Tk);
+          const int q = (Tk.ny + Tl.ny + 3 * part) & 3;
+          double half = readout(v, xa, pl, t, Tl, q);
+          deposit(cl + part, (q == 1 || q == 2) ? -half : half);
         }
-        const int q = (Tk.ny + Tl.ny + 3 * da.part) & 3;
-        double half = readout(v, xa, pl, t, Tl, q);
-        half *= (q == 1 || q == 2) ? -scale : scale;
-        deposit(cl, half);
-        cl += 1;
       }
     }
     __syncthreads();

@@ -114,16 +114,18 @@ def test_workspace_size_arguments(lib):
 
 
 def test_shard_ranges_tile_the_circuits(lib):
+    """Blocks of whole tasks (even boundaries: the Re and Im circuits of a task stay on one rank)
+    tile [0, C) and differ by at most one task (plus the odd circuit of an odd C)."""
     for C in (0, 1, 7, 2560, 90112, 360448):
         for W in (1, 2, 3, 4, 8):
             prev = 0
             sizes = []
             for r in range(W):
                 a, b = dvqls.dvqls_shard_range(C, r, W)
-                assert a == prev
+                assert a == prev and a % 2 == 0
                 prev = b
                 sizes.append(b - a)
-            assert prev == C and max(sizes) - min(sizes) <= 1
+            assert prev == C and max(sizes) - min(sizes) <= 2 + (C % 2)
     with pytest.raises(dvqls.DvqlsError):
         dvqls.dvqls_shard_range(10, 2, 2)
 
