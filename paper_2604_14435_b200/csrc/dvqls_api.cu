@@ -713,7 +713,12 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
     dvqls_shard_range(ctx->C, ctx->vrank, ctx->vworld, &ctx->c0, &ctx->c1);
   else
     dvqls_shard_range(ctx->C, ctx->rank, ctx->world, &ctx->c0, &ctx->c1);
-  ctx->chunk = (ctx->C + ctx->world - 1) / ctx->world;
+  ctx->chunk = 0;  // the largest rank block (terms buffer and allgather slot)
+  for (int r = 0; r < std::max(ctx->world, ctx->vworld); ++r) {
+    int64_t a, b;
+    dvqls_shard_range(ctx->C, r, std::max(ctx->world, ctx->vworld), &a, &b);
+    ctx->chunk = std::max(ctx->chunk, b - a);
+  }
   if (ctx->c1 - ctx->c0 > int64_t(INT32_MAX)) {  // the kernels index a rank's circuits with 32-bit ints
     fail(ctx, DVQLS_E_UNSUPPORTED, "%lld circuits on one rank (more than 2^31 - 1): use more ranks",
          (long long)(ctx->c1 - ctx->c0));
@@ -1129,7 +1134,8 @@ int dvqls_terms(dvqls_ctx* ctx, const double* theta, double* out) {
   } else if (ctx->comm) {
     CKN(nccl().AllGather(ctx->d_terms, ctx->d_gather, size_t(ctx->chunk), ncclDouble, ctx->comm, ctx->stream));
     for (int r = 0; r < ctx->world; ++r) {
-      const int64_t a = ctx->C * r / ctx->world, b = ctx->C * (r + 1) / ctx->world;
+      int64_t a, b;
+      dvqls_shard_range(ctx->C, r, ctx->world, &a, &b);
       CK(cudaMemcpyAsync(out + a, ctx->d_gather + size_t(r) * ctx->chunk, sizeof(double) * (b - a),
                          cudaMemcpyDeviceToHost, ctx->stream));
     }
@@ -1139,7 +1145,8 @@ int dvqls_terms(dvqls_ctx* ctx, const double* theta, double* out) {
     CK(cudaStreamSynchronize(ctx->stream));
     if ((rc = all_gather_host(ctx, mine.data(), all.data(), sizeof(double) * ctx->chunk))) return rc;
     for (int r = 0; r < ctx->world; ++r) {
-      const int64_t a = ctx->C * r / ctx->world, b = ctx->C * (r + 1) / ctx->world;
+      int64_t a, b;
+      dvqls_shard_range(ctx->C, r, ctx->world, &a, &b);
       std::memcpy(out + a, all.data() + size_t(r) * ctx->chunk, sizeof(double) * (b - a));
     }
   }
