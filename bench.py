@@ -587,7 +587,7 @@ def main():
     if w.n > 12:
         roof = streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, ctx.grid())
     else:
-        kern = (("plane2_kernel" if args.variant == 2 else "plane_kernel<20>") if w.n == 10 and w.bkind == 0 else
+        kern = (("plane_kernel<20>" if args.variant == 1 else "plane2_kernel") if w.n == 10 and w.bkind == 0 else
                 f"onchip_plane_kernel<{w.n}>" if w.n > 10 and w.bkind == 0 else
                 "stream_hadamard_kernel<HH>" if w.n > 10 else "hadamard_kernel")
         roof = onchip_roofline(w, local_c, KT, had_ms, sms, fmax, peak_src, kern)

@@ -126,9 +126,10 @@ typedef struct dvqls_opts {
   int stage;                   /* n >= 13 uniform b: TMA staging of streaming tiles. 0 = from
                                   n = 16 (default), -1 = off, 1 = from n = 13                   */
   int stream_grid;             /* n >= 11: cap on the CTAs of the streaming kernels (0 = one wave) */
-  int variant;                 /* kernel variant for n = 10, uniform b: 0 = default, 1 = one circuit
-                                  per warp (plane_kernel), 2 = two circuits in flight per warp
-                                  (plane2_kernel).  Same circuits and results to rounding.     */
+  int variant;                 /* kernel variant for n = 10, uniform b: 0 = default (= 2), 1 = one
+                                  circuit per warp (plane_kernel), 2 = two circuits in flight per
+                                  warp, skewed phases (plane2_kernel; measured 0.6-1.5 % faster).
+                                  Bitwise-identical terms; (E, Psi) equal to rounding.          */
   int prefix;                  /* V(theta)|0> for 7 <= n <= 10: 0 = one CTA per theta (default);
                                   1 = a thread-block cluster of 2^(n-7) CTAs per theta joined by
                                   DSMEM (measured no faster on B200: DESIGN.md §6)              */

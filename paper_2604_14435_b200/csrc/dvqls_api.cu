@@ -676,7 +676,7 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
   if (n <= kMaxRegQubits) {
     ctx->path = Path::reg;
     if (n == 10 && !hh)
-      ctx->kc = o.variant == 2 ? plane2_cfg() : plane_cfg();
+      ctx->kc = o.variant == 1 ? plane_cfg() : plane2_cfg();  // default: two circuits per warp
     else
       ctx->kc = n <= 6 ? reg_cfg_lo(n, hh) : reg_cfg_hi(n, hh);
   } else if (hh) {
