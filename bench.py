@@ -337,11 +337,12 @@ def main():
         pbuild.build()
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        obj = [dvqls.dvqls_nccl_unique_id() if rank == 0 else None]
+        # one ncclUniqueId per communicator (the measured context, the probe context, NEXT-2's)
+        obj = [[dvqls.dvqls_nccl_unique_id() for _ in range(3)] if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        nccl_ids = obj[0]
     else:
-        nccl_id = None
+        nccl_ids = [None, None, None]
 
     stream = torch.cuda.Stream(device=dev)
     KT = args.batch
@@ -353,7 +354,7 @@ def main():
             raise SystemExit("--slice is the 1-GPU weak-scaling reference")
         vopts.update(virtual_rank=0, virtual_world=args.slice)
 
-    def make_ctx(timing):
+    def make_ctx(timing, nccl_id):
         # device memory comes from torch: the library carves its tables from this workspace
         ws_bytes = dvqls.workspace_size(w.n, w.layers, w.L, device=local, rank=rank, world=world,
                                         max_batch=max(KT, 1), **{k: v for k, v in vopts.items() if k not in ("graphs", "variant")})
@@ -362,8 +363,8 @@ def main():
                              nccl_id=nccl_id, entangler=w.entangler, stream=stream, timing=timing,
                              max_batch=max(KT, 1), workspace=workspace, **vopts)
 
-    ctx = make_ctx(False)   # the measured path: CUDA graph per call, PDL between prefix and kernel
-    pctx = make_ctx(True)   # probe: CUDA events between the kernels (per-kernel times, roofline)
+    ctx = make_ctx(False, nccl_ids[0])   # the measured path: CUDA graph per call, PDL between prefix and kernel
+    pctx = make_ctx(True, nccl_ids[1])   # probe: CUDA events between the kernels (per-kernel times, roofline)
     c0, c1 = ctx.local_range()
     thetas = np.stack([w.theta0(s) for s in range(KT)])
     th_dev = torch.tensor(thetas, dtype=torch.float64, device=dev)
@@ -523,7 +524,7 @@ def main():
     next2 = None
     if w.bkind == 0 and not args.no_next2 and args.slice <= 1:
         nctx = dvqls.Context(w.n, w.layers, chars, co, w.bkind, w.b, device=local, rank=rank, world=world,
-                             nccl_id=nccl_id, entangler=w.entangler, stream=stream, timing=False,
+                             nccl_id=nccl_ids[2], entangler=w.entangler, stream=stream, timing=False,
                              max_batch=max(KT, 1), mode=dvqls.DVQLS_MODE_PAULI)
         p_steps = max(3, args.steps // 4)
         with torch.cuda.stream(stream):

@@ -33,7 +33,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    obj = [dvqls.dvqls_nccl_unique_id() if rank == 0 else None]
+    obj = [dvqls.dvqls_nccl_unique_id() if rank == 0 else None, dvqls.dvqls_nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     w = {"cfg1": configs.cfg1, "cfg3": configs.cfg3, "cfg2p": configs.cfg2_pressure,
          "n12": lambda: configs.random_workload(12, 2, 2, seed=77)}[args.config]()
@@ -45,9 +45,14 @@ def main():
     cb, _ = ctx.cost_batch(ths)
     CLg, CG, _, _ = ctx.global_cost(th)
     c0, c1 = ctx.local_range()
+    # a second context of the same ranks (its own communicator, NCCL reduction path) alongside
+    ctx2 = dvqls.from_workload(w, device=local, rank=rank, world=world, nccl_id=obj[1], mode=args.mode,
+                               allreduce=dvqls.DVQLS_ALLREDUCE_NCCL)
+    C2 = ctx2.cost(th)
+    ctx2.destroy()
     ok = True
     # every rank must hold identical global results
-    t = torch.tensor([C, cb[0], cb[1], cb[2], float(terms.sum()), CG], dtype=torch.float64, device="cuda")
+    t = torch.tensor([C, cb[0], cb[1], cb[2], float(terms.sum()), CG, C2], dtype=torch.float64, device="cuda")
     lst = [torch.zeros_like(t) for _ in range(world)]
     dist.all_gather(lst, t)
     if rank == 0:
@@ -59,7 +64,7 @@ def main():
         refb = [ocost.cost(sim.workload_terms(w, ths[k]), ocost.coeffs_of(w), w.n, w.L)[0] for k in range(3)]
         same = all(torch.equal(lst[0], x) for x in lst)
         CGr = ocost.global_cost(sim.workload_overlaps(w, th), ocost.coeffs_of(w), Pr)
-        ok = (err <= 1e-10 and abs(C - Cr) <= 1e-10 and max(abs(cb[k] - refb[k]) for k in range(3)) <= 1e-10
+        ok = (err <= 1e-10 and abs(C - Cr) <= 1e-10 and abs(C2 - Cr) <= 1e-10 and max(abs(cb[k] - refb[k]) for k in range(3)) <= 1e-10
               and same and abs(CG - CGr) <= 1e-10 and abs(CLg - Cr) <= 1e-10)
         print(f"world={world} mode={args.mode} {w.name}: max|term err|={err:.2e} C={C:.12f} oracle={Cr:.12f} "
               f"C_G={CG:.12f} oracle={CGr:.12f} "
