@@ -11,6 +11,6 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/$
 B="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-next2"
 timeout 300 $B > gpurun_out/${TAG}_b5.json 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"plane_kernel" -c 1 -o gpurun_out/${TAG}_prof $B > gpurun_out/${TAG}_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"plane2_kernel" -c 1 -o gpurun_out/${TAG}_prof $B > gpurun_out/${TAG}_ncu.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"prefix_quad" -c 1 -o gpurun_out/${TAG}_prefix $B > gpurun_out/${TAG}_ncu_prefix.log 2>&1
 echo done
