@@ -52,7 +52,7 @@ def launches(path):
             elif r[ui] in ("msecond", "ms"):
                 v *= 1e6
             d[re.sub(r"\(.*", "", r[ki])[:70]].append(v)
-    ours = re.compile(r"dvqls|plane::|streamp::|stream::|pauli::|decomp::|glob::|tile::")
+    ours = re.compile(r"dvqls|plane::|plane2::|pclus::|onchip::|streamp::|stream::|pauli::|decomp::|glob::|tile::|shift::")
     tot = sum(sum(v) for k, v in d.items() if ours.search(k))
     print(f"{'kernel':70s} {'launches':>8s} {'mean us':>10s} {'share of dvqls time':>20s}")
     for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
