@@ -45,7 +45,7 @@ KernelCfg plane2_cfg() {
   return k;
 }
 
-PrefixCfg prefix_cfg(int n, int layers, int cluster) {
+PrefixCfg prefix_cfg(int n, int layers, bool cluster) {
   static const void* quads[11] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                                   (const void*)&prefix_quad_kernel<7>, (const void*)&prefix_quad_kernel<8>,
                                   (const void*)&prefix_quad_kernel<9>, (const void*)&prefix_quad_kernel<10>};
@@ -61,34 +61,12 @@ PrefixCfg prefix_cfg(int n, int layers, int cluster) {
                                  sizeof(double2) * pclus::smem_doubles2<10>(1)};
   PrefixCfg p;
   const size_t N = size_t(1) << n;
-  // two-level cluster variants (prefix_cluster2_kernel): 2 (cluster == 2) or 4 (cluster == 3) CTAs
-  if ((cluster == 2 || cluster == 3) && n >= 8 && n <= 10) {
-    const int CB = cluster == 2 ? 1 : 2;
-    if (n - CB >= 7) {
-      static const void* k1[11] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                   (const void*)&pclus::prefix_cluster2_kernel<8, 1>,
-                                   (const void*)&pclus::prefix_cluster2_kernel<9, 1>,
-                                   (const void*)&pclus::prefix_cluster2_kernel<10, 1>};
-      static const void* k2[11] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                   (const void*)&pclus::prefix_cluster2_kernel<9, 2>,
-                                   (const void*)&pclus::prefix_cluster2_kernel<10, 2>};
-      const size_t per_layer = sizeof(double2) * (2 * size_t(n) + (size_t(1) << (2 * CB)));
-      const size_t bytes = sizeof(double2) * 3 * (N >> CB) + per_layer * size_t(layers);
-      if (bytes <= size_t(200) << 10) {
-        p.fn = CB == 1 ? k1[n] : k2[n];
-        p.threads = int((N >> CB) / 4);
-        p.smem = bytes;
-        p.cluster = 1 << CB;
-        return p;
-      }
-    }
-  }
   // cluster: 7 <= n <= 10, the state spread over 2^(n-7) CTAs joined by DSMEM (one amplitude per
   // thread), while its tables fit the SMEM of one CTA (they grow with the depth).  Measured at cfg3
   // (profiles/r2_cluster_prefix/): 20-24 us vs 21-23 us for the one-CTA kernel -- the per-layer
   // cluster barrier (~0.9 K cycles with skew) and the 8x-redundant DSMEM gather (~1-1.6 K cycles)
   // cost what the 8 SMs save -- so it is the opt-in variant (opts.prefix = 1).
-  if (cluster == 1 && n >= 7 && n <= 10) {
+  if (cluster && n >= 7 && n <= 10) {
     const size_t per_layer = csm[n] - sizeof(double2) * 3 * pclus::NL;
     const size_t bytes = sizeof(double2) * 3 * pclus::NL + per_layer * size_t(layers);
     if (bytes <= size_t(200) << 10) {

@@ -187,174 +187,3 @@ prefix_cluster_kernel(int layers, int entangler, const double* __restrict__ thet
 
 }  // namespace pclus
 }  // namespace dvqls
-
-namespace dvqls {
-namespace pclus {
-
-// ---------------------------------------------------------------------------------------------
-// Two-level variant: 2^CB CTAs (CB = 1 or 2) of 2^(LB-2) threads x 4 amplitudes, LB = n - CB local
-// bits, the one-CTA quad layout inside each CTA (prefix_quad_kernel):
-//   layout X: local j = (w << 7) | (l << 2) | r   (r: positions 0, 1; lane l: 2..6; warp w: 7..LB-1)
-//   layout Y: warp bits <-> lane bits 0..W-1 (positions 7..LB-1 become lane bits)
-// Per layer: register + lane gates in X, one SMEM transpose to Y, lane gates on positions 7..LB-1,
-// publish Y, one cluster barrier, then each output amplitude (layout X) gathers its 2^CB sources
-// of the ring and cluster-bit gates over DSMEM: each amplitude is read by 2^CB CTAs (2x or 4x),
-// not 8x as in prefix_cluster_kernel.
-// ---------------------------------------------------------------------------------------------
-template <int NQ, int CB>
-struct PC2 {
-  static constexpr int CS = 1 << CB;
-  static constexpr int LB = NQ - CB;
-  static constexpr int NLOC = 1 << LB;       // amplitudes per CTA
-  static constexpr int THREADS = NLOC / 4;   // 4 amplitudes per thread
-  static constexpr int W = LB - 7;           // warp bits
-};
-
-__device__ __forceinline__ int q2swz(int j) { return j ^ ((j >> 2) & 7) ^ ((j >> 7) & 7); }
-
-// dynamic SMEM (double2): gates 2G | cluster tables CS^2 per layer | transpose NLOC | publish 2 NLOC
-template <int NQ, int CB>
-__host__ __device__ constexpr size_t smem2_doubles2(int layers) {
-  return size_t(2) * NQ * layers + size_t(PC2<NQ, CB>::CS) * PC2<NQ, CB>::CS * layers + 3 * PC2<NQ, CB>::NLOC;
-}
-
-template <int NQ, int CB>
-__global__ void __launch_bounds__(PC2<NQ, CB>::THREADS)
-prefix_cluster2_kernel(int layers, int entangler, const double* __restrict__ thetas, double2* __restrict__ x_all) {
-  pdl_trigger();
-  using S = PC2<NQ, CB>;
-  constexpr int n = NQ, CS = S::CS, LB = S::LB, NLOC = S::NLOC, W = S::W;
-  static_assert(W >= 0 && W <= 5, "layout needs 7 <= LB <= 12");
-  extern __shared__ double2 pcsm[];
-  const int G = n * layers;
-  double2* U = pcsm;                       // 2 per gate
-  double2* GC = U + 2 * G;                 // [layer][c][c']
-  double2* sbuf = GC + CS * CS * layers;   // NLOC (transpose X -> Y)
-  double2* pub = sbuf + NLOC;              // [2][NLOC] published Y-layout amplitudes (swizzled)
-  const double* th = thetas + (size_t)blockIdx.y * 3 * G;
-  const int tid = threadIdx.x, l = tid & 31, w = tid >> 5;
-  const uint32_t rank = cta_rank();
-  const unsigned full = 0xffffffffu;
-
-  for (int g = tid; g < G; g += S::THREADS) {
-    double s0, c0, s1, c1, s2, c2;
-    sincos(0.5 * th[3 * g + 0], &s0, &c0);
-    sincos(0.5 * th[3 * g + 1], &s1, &c1);
-    sincos(0.5 * th[3 * g + 2], &s2, &c2);
-    U[2 * g + 0] = make_double2(c1 * (c2 * c0 - s2 * s0), -s1 * (c2 * c0 + s2 * s0));
-    U[2 * g + 1] = make_double2(c1 * (s2 * c0 + c2 * s0), s1 * (c2 * s0 - s2 * c0));
-  }
-  __syncthreads();
-  for (int e = tid; e < CS * CS * layers; e += S::THREADS) {  // cluster bit b = position LB + b
-    const int layer = e / (CS * CS), rc = e % (CS * CS), c = rc / CS, cp = rc % CS;
-    double2 f = make_double2(1.0, 0.0);
-    for (int b = 0; b < CB; ++b) f = cmul(f, uent(U, layer * n + (n - 1 - (LB + b)), (c >> b) & 1, (cp >> b) & 1));
-    GC[e] = f;
-  }
-  // this thread's 4 amplitudes in layout X and their ring sources
-  const int jX0 = (w << 7) | (l << 2);
-  const int jY0 = ((l >> W) << (2 + W)) | (w << 2) | ((l & ((1 << W) - 1)) << 7);
-  const uint32_t pub_base = uint32_t(__cvta_generic_to_shared(pub));
-  uint32_t remote[CS];
-#pragma unroll
-  for (int c = 0; c < CS; ++c) remote[c] = mapa(pub_base, uint32_t(c));
-  uint32_t src_off[4];  // byte offset of the ring source's local slot
-  uint32_t src_c[4];    // its CTA (cluster bits)
-  bool neg[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const uint32_t i = (rank << LB) | uint32_t(jX0 | r);
-    uint32_t p = i;
-    neg[r] = false;
-    if (entangler == 0) {
-#pragma unroll
-      for (int q = n - 1; q >= 0; --q) {
-        const int pc = n - 1 - q, pt = n - 1 - ((q + 1) % n);
-        if ((p >> pc) & 1u) p ^= 1u << pt;
-      }
-    } else {
-      int par = 0;
-#pragma unroll
-      for (int q = 0; q < n; ++q) par ^= int((i >> (n - 1 - q)) & (i >> (n - 1 - (q + 1) % n))) & 1;
-      neg[r] = par;
-    }
-    src_c[r] = p >> LB;
-    src_off[r] = uint32_t(q2swz(int(p & uint32_t(NLOC - 1)))) * 16u;
-  }
-  __syncthreads();  // tables ready
-
-  double2 v[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) v[r] = make_double2((rank == 0 && (jX0 | r) == 0) ? 1.0 : 0.0, 0.0);
-
-  auto reg_gate = [&](int g, int rbit) {
-    const double2 ua = U[2 * g], ub = U[2 * g + 1];
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-      if (!(r & (1 << rbit))) {
-        const double2 x0 = v[r], x1 = v[r | (1 << rbit)];
-        v[r] = make_double2(fma(ua.x, x0.x, fma(-ua.y, x0.y, fma(-ub.x, x1.x, -ub.y * x1.y))),
-                            fma(ua.x, x0.y, fma(ua.y, x0.x, fma(-ub.x, x1.y, ub.y * x1.x))));
-        v[r | (1 << rbit)] = make_double2(fma(ub.x, x0.x, fma(-ub.y, x0.y, fma(ua.x, x1.x, ua.y * x1.y))),
-                                          fma(ub.x, x0.y, fma(ub.y, x0.x, fma(ua.x, x1.y, -ua.y * x1.x))));
-      }
-  };
-  auto lane_gate = [&](int g, int lbit) {
-    const double2 ua = U[2 * g], ub = U[2 * g + 1];
-    const bool bit = (l >> lbit) & 1;
-    const double2 cs = make_double2(ua.x, bit ? -ua.y : ua.y);
-    const double2 co = make_double2(bit ? ub.x : -ub.x, ub.y);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const double2 pp =
-          make_double2(__shfl_xor_sync(full, v[r].x, 1 << lbit), __shfl_xor_sync(full, v[r].y, 1 << lbit));
-      const double sr = fma(cs.x, v[r].x, -cs.y * v[r].y), si = fma(cs.x, v[r].y, cs.y * v[r].x);
-      v[r] = make_double2(fma(co.x, pp.x, fma(-co.y, pp.y, sr)), fma(co.x, pp.y, fma(co.y, pp.x, si)));
-    }
-  };
-
-  for (int layer = 0; layer < layers; ++layer) {
-    const int gl = layer * n;  // gate of qubit q is gl + q, qubit q <-> position n - 1 - q
-    reg_gate(gl + (n - 1 - 0), 0);
-    reg_gate(gl + (n - 1 - 1), 1);
-#pragma unroll
-    for (int pos = 2; pos < 7; ++pos) lane_gate(gl + (n - 1 - pos), pos - 2);
-    double2* P = pub + (layer & 1) * NLOC;
-    if (W > 0) {  // X -> Y through SMEM, gates on the warp positions, publish Y
-#pragma unroll
-      for (int r = 0; r < 4; ++r) sbuf[q2swz(jX0 | r)] = v[r];
-      __syncthreads();
-#pragma unroll
-      for (int r = 0; r < 4; ++r) v[r] = sbuf[q2swz(jY0 | r)];
-#pragma unroll
-      for (int pos = 7; pos < LB; ++pos) lane_gate(gl + (n - 1 - pos), pos - 7);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) P[q2swz(jY0 | r)] = v[r];
-    } else {
-#pragma unroll
-      for (int r = 0; r < 4; ++r) P[q2swz(jX0 | r)] = v[r];
-    }
-    cluster_barrier();  // every CTA's layer is published (and the transpose buffer is free again)
-    // ring + cluster-bit gates: out[i] = sign * sum_c' GC[c(p)][c'] S_c'[j(p)],  p = ring(i)
-    const uint32_t par = uint32_t(layer & 1) * uint32_t(NLOC * 16);
-    const double2* gcl = GC + CS * CS * layer;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      double2 src[CS];
-#pragma unroll
-      for (int c = 0; c < CS; ++c) src[c] = ld_dsmem(remote[c] + par + src_off[r]);
-      const double2* gc = gcl + CS * src_c[r];
-      double2 acc = cmul(gc[0], src[0]);
-#pragma unroll
-      for (int c = 1; c < CS; ++c) acc = cmac(gc[c], src[c], acc);
-      v[r] = neg[r] ? make_double2(-acc.x, -acc.y) : acc;
-    }
-  }
-  double2* x = x_all + (size_t)blockIdx.y * (1u << n) + (size_t(rank) << LB);
-#pragma unroll
-  for (int r = 0; r < 4; ++r) x[jX0 | r] = v[r];
-  cluster_barrier();  // peers may still read this CTA's last published layer
-}
-
-}  // namespace pclus
-}  // namespace dvqls

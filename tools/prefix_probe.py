@@ -22,7 +22,7 @@ w = configs.cfg3()
 th = torch.tensor(np.stack([w.theta0(s) for s in range(K)]), dtype=torch.float64, device="cuda")
 out = torch.empty(5 * K, dtype=torch.float64, device="cuda")
 res = {}
-for name, pf in (("one_cta", 0), ("cluster8_flat", 1), ("cluster2", 2), ("cluster4", 3)):
+for name, pf in (("cluster", 1), ("one_cta", 0)):
     ctx = dvqls.from_workload(w, max_batch=K, timing=True, prefix=pf)
     ms = []
     for i in range(30):
