@@ -389,12 +389,16 @@ def main():
         # contains a cross-rank reduction) until >= min_s of load so the SM clock has ramped
         t_w = time.time()
         i = 0
+        chunk = 8
         while True:
-            for _ in range(8):
+            t_c = time.time()
+            for _ in range(chunk):
                 flush.zero_()
                 c.cost_dev(K, th_dev, out_dev)
                 i += 1
             torch.cuda.synchronize()
+            if time.time() - t_c > 1.0:
+                chunk = 1  # long steps (cfg5 at large n): warm up one call at a time
             more = 1.0 if (i < args.warmup or time.time() - t_w < min_s) else 0.0
             if world > 1:
                 t = torch.tensor([more], device=dev)

@@ -5,6 +5,6 @@ for N in ${NS:-12 14 16 18 20}; do
 done
 if [ "${NCU:-1}" = "1" ]; then
 B="python bench.py --config cfg5 --n ${NCUN:-16} --batch 2 --steps 1 --warmup 3 --no-cpu-baseline"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tile_hadamard" -c 1 -o gpurun_out/${TAG}_prof $B > gpurun_out/${TAG}_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"stream_plane_kernel" -c 1 -o gpurun_out/${TAG}_prof $B > gpurun_out/${TAG}_ncu.log 2>&1
 fi
 echo done
