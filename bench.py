@@ -514,14 +514,15 @@ def main():
             terms, nrm, ms = dvqls.decompose(A, 0.01, device=local, timing=True)
             best = ms if best is None else min(best, ms)
         byts = 16 * 4 ** nd      # algorithmic: A read once (any decomposition must)
-        moved = 48 * 4 ** nd     # this design: A read, XOR-diagonal rows B written and read once
+        moved = 16 * 4 ** nd     # this design: the XOR diagonals gathered straight from A (round 1: 48 * 4^n)
         pk = float(load_peaks()[0]["hbm_gbs"])
         next4 = {"n": nd, "terms": len(terms), "ms": best, "GBps": byts / (best * 1e-3) / 1e9,
                  "hbm_frac": byts / (best * 1e-3) / 1e9 / pk,
                  "moved_GBps": moved / (best * 1e-3) / 1e9, "moved_frac": moved / (best * 1e-3) / 1e9 / pk,
-                 "note": ("NEXT-4: 4^n coefficients by per-x-mask FWHT in one candidate pass (Parseval bound; exact "
-                          "norm filter in the sort) + sort on the GPU; GBps = algorithmic bytes 16*4^n (A read once) "
-                          "over the device time (best of 3); moved_GBps = the 48*4^n bytes this design moves")}
+                 "note": ("NEXT-4: 4^n coefficients by one FWHT per x-mask of the XOR diagonal gathered from A, one "
+                          "candidate pass (Parseval bound from ||A||_F^2 summed during the upload; exact norm filter "
+                          "in the sort) + sort on the GPU; GBps = algorithmic bytes 16*4^n (A read once) over the "
+                          "device time after the upload (best of 3)")}
         del A
 
     # ---- NEXT-2 algebraic fast path (flagged; reported separately, never the headline) ----------

@@ -5,17 +5,19 @@
 //
 // P(m, z)|k> = i^{popcount(m&z)} (-1)^{popcount(k&z)} |k ^ m> has one nonzero per column, so for a
 // fixed x-mask m the 2^n coefficients are one Walsh-Hadamard transform (over k) of the "XOR
-// diagonal" a_m[k] = A[k, k ^ m].  xor_transpose_kernel lays the diagonals out as contiguous
-// rows B[m, :] (coalesced tiles) and sums |A|^2 on the way; then one CTA per m runs the FWHT
-// (n >= 9: 16 amplitudes per thread in registers, ceil(n/4) register passes joined by SMEM
-// exchanges; n <= 8: radix-2 in SMEM), phase and scale.
+// diagonal" a_m[k] = A[k, k ^ m].  One CTA per m gathers its diagonal straight from A (element k
+// from row k: a 16-byte read per row; the CTAs of m, m^1, ..., m^7 -- launched together -- read the
+// same 128-byte line of each row, so DRAM delivers A once), runs the FWHT (n >= 9: 16 amplitudes per
+// thread in registers, ceil(n/4) register passes joined by SMEM exchanges; n <= 8: radix-2 in SMEM),
+// phase and scale.  Round 1 wrote the diagonals as rows of a second matrix B first (A read, B
+// written, B read: 48 * 4^n bytes); this reads A once (16 * 4^n).
 //
-// One pass over B: Parseval, sum_P |c_P|^2 = ||A||_F^2 / 2^n, gives ||c||_2 before the FWHT up to
-// rounding, so the pass compacts every CANDIDATE |c| >= max(1e-14, eps ||A||_F / 2^{n/2} (1 - 1e-9))
-// and, in the same pass, sums |c|^2 per row in a fixed order; the exact ||c||_2 = sqrt(sum |c|^2)
-// (the definition, reading 15) then applies the pruning rule to the candidates inside the sort.
-// Traffic: A read, B written, B read = 48 * 4^n bytes, coalesced, HBM-bound; no 4^n coefficient
-// array is stored.
+// Pruning needs ||c||_2 before the pass that compacts survivors.  Parseval, sum_P |c_P|^2 =
+// ||A||_F^2 / 2^n, gives it up to rounding, and ||A||_F^2 is summed row block by row block as A is
+// uploaded (fro_rows_kernel after each chunk of the host-to-device copy, while the chunk is in L2),
+// so ONE pass compacts every CANDIDATE |c| >= max(1e-14, eps ||A||_F / 2^{n/2} (1 - 1e-9)) and, in
+// the same pass, sums |c|^2 per row in a fixed order; the exact ||c||_2 = sqrt(sum |c|^2) (the
+// definition, reading 15) then applies the pruning rule to the candidates inside the sort.
 //
 // Pruning keeps |c| >= 1e-14 and |c| >= eps * ||c||_2 (reading 15); survivors are sorted by
 // (round(|c| / (1e-12 ||c||_2)) descending, lexicographic I<X<Y<Z ascending) in one CTA.
@@ -35,59 +37,26 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 constexpr int SORT_MAX = 4096;
 constexpr size_t SORT_SMEM = SORT_MAX * (8 + 8 + 4);
 
-// XOR-diagonal transposition B[m, k] = A[k, k ^ m] in 32 x 32 tiles: the tile of rows
-// [k0, k0+32) x columns [j0, j0+32) holds exactly the elements of B rows M0 + (a ^ b) (M0 =
-// (k0 ^ j0) & ~31), columns k0 + a; read along j and written along k, both coalesced.
-// Persistent over the 32 x 32 tiles; fro[cta] = sum of |A|^2 over the CTA's tiles (fixed order),
-// for the Parseval candidate bound.
-__global__ void __launch_bounds__(256) xor_transpose_kernel(const double2* __restrict__ A, int n,
-                                                            double2* __restrict__ B, double* __restrict__ fro) {
-  __shared__ double2 t[32][33];
+// |A|^2 of rows [r0, r0 + gridDim.x * rows_per_cta): CTA b sums its rows in a fixed order into
+// fro[r0 / rows_per_cta + b] (run after each chunk of the upload, on the chunk just copied)
+__global__ void __launch_bounds__(256) fro_rows_kernel(const double2* __restrict__ A, uint32_t N, uint32_t r0,
+                                                       uint32_t rows_per_cta, double* __restrict__ fro) {
   __shared__ double red[8];
-  const uint32_t N = 1u << n, tiles = N >> 5;
-  const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const size_t base = (size_t(r0) + size_t(blockIdx.x) * rows_per_cta) * N;
+  const uint32_t cnt = rows_per_cta * N;
   double acc = 0.0;
-  for (uint32_t tile = blockIdx.x; tile < tiles * tiles; tile += gridDim.x) {  // persistent
-    const uint32_t k0 = (tile / tiles) << 5, j0 = (tile % tiles) << 5;
-    {  // bulk-prefetch the next tile's 32 row segments (512 B each) into L2
-      const uint32_t nt = tile + gridDim.x;
-      if (nt < tiles * tiles && threadIdx.x < 32)
-        prefetch_l2(A + size_t(((nt / tiles) << 5) + threadIdx.x) * N + ((nt % tiles) << 5), 512u);
-    }
-    __syncthreads();  // previous tile's readers of t are done
-    for (uint32_t r = ty; r < 32; r += 8) {
-      const double2 a = __ldcs(A + size_t(k0 + r) * N + j0 + tx);
-      acc = fma(a.x, a.x, fma(a.y, a.y, acc));
-      t[r][tx] = a;
-    }
-    __syncthreads();
-    const uint32_t M0 = (k0 ^ j0) & ~31u;
-    for (uint32_t ml = ty; ml < 32; ml += 8)  // row M0 + ml of B gets A[k0 + tx, j0 + (tx ^ ml)]
-      B[size_t(M0 + ml) * N + k0 + tx] = t[tx][tx ^ ml];
+  for (uint32_t i = threadIdx.x; i < cnt; i += 256) {
+    const double2 a = __ldcg(A + base + i);
+    acc = fma(a.x, a.x, fma(a.y, a.y, acc));
   }
   for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (tx == 0) red[ty] = acc;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     double f = 0.0;
     for (int w = 0; w < 8; ++w) f += red[w];
-    fro[blockIdx.x] = f;
+    fro[r0 / rows_per_cta + blockIdx.x] = f;
   }
-}
-
-// n < 5 (no transposition): fro[0] = sum |A|^2, one CTA
-__global__ void __launch_bounds__(256) fro_small_kernel(const double2* __restrict__ A, uint32_t NN,
-                                                        double* __restrict__ fro) {
-  __shared__ double red[256];
-  double acc = 0.0;
-  for (uint32_t i = threadIdx.x; i < NN; i += 256) acc = fma(A[i].x, A[i].x, fma(A[i].y, A[i].y, acc));
-  red[threadIdx.x] = acc;
-  __syncthreads();
-  for (int off = 128; off >= 1; off >>= 1) {
-    if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) fro[0] = red[0];
 }
 
 // candidate threshold from Parseval: thr0 = eps * sqrt(sum fro / 2^n) * (1 - 1e-9) (below the
@@ -153,18 +122,17 @@ __device__ __forceinline__ void row_sq(double acc, double* __restrict__ sq, doub
   }
 }
 
-// n <= 8: radix-2 FWHT of row m in SMEM (n < 5: the diagonal read straight from A)
+// n <= 8: radix-2 FWHT of the XOR diagonal m of A in SMEM
 template <int MODE>
 __global__ void __launch_bounds__(THREADS)
-fwht_rows_kernel(const double2* __restrict__ B, int n, double2* __restrict__ C, double* __restrict__ sq,
+fwht_rows_kernel(const double2* __restrict__ A, int n, double2* __restrict__ C, double* __restrict__ sq,
                  const double* __restrict__ thrf2, uint64_t cap, unsigned long long* __restrict__ count,
-                 uint64_t* __restrict__ idx, int direct) {
+                 uint64_t* __restrict__ idx) {
   extern __shared__ double2 rows_smem[];  // dynamic: 2^n amplitudes
   constexpr int NV = 1;
   const uint32_t N = 1u << n;
   const uint32_t m0 = blockIdx.x;
-  for (uint32_t k = threadIdx.x; k < N; k += THREADS)
-    rows_smem[k] = direct ? __ldg(B + size_t(k) * N + (k ^ m0)) : __ldg(B + size_t(m0) * N + k);
+  for (uint32_t k = threadIdx.x; k < N; k += THREADS) rows_smem[k] = __ldcg(A + size_t(k) * N + (k ^ m0));
   __syncthreads();
   for (int b = 0; b < n; ++b) {  // radix-2 stages; (a, b) -> (a + b, a - b)
     const uint32_t h = 1u << b;
@@ -186,11 +154,11 @@ fwht_rows_kernel(const double2* __restrict__ B, int n, double2* __restrict__ C, 
   if (MODE == 1) row_sq<THREADS>(acc, sq, inv, blockIdx.x);
 }
 
-// n = NB >= 9: row m of B in registers, RG = 16 amplitudes per thread (2^(NB-4) threads).
+// n = NB >= 9: XOR diagonal m of A in registers, RG = 16 amplitudes per thread (2^(NB-4) threads).
 // Pass g puts index bits [b_g, b_g + 4) in registers (b_0 = NB - 4, b_1 = NB - 8, ..., last 0)
 // and butterflies the bits of that window not done before; consecutive passes exchange through
-// SMEM (slot(i) = i ^ ((i >> 4) & 7): conflict-free LDS.128/STS.128 in every layout).  Global
-// loads (pass 0 layout, i = r << (NB - 4) | t) are coalesced; HBM traffic = one read of the row.
+// SMEM (slot(i) = i ^ ((i >> 4) & 7): conflict-free LDS.128/STS.128 in every layout).  Element k
+// of the diagonal is A[k, k ^ m] (pass 0 layout, k = r << (NB - 4) | t: one 16-byte read per row).
 constexpr int RG = 16;
 template <int NB>
 __device__ __forceinline__ uint32_t rows_idx(uint32_t t, uint32_t r, int b) {
@@ -200,7 +168,7 @@ __device__ __forceinline__ uint32_t rows_slot(uint32_t i) { return i ^ ((i >> 4)
 
 template <int NB, int MODE>
 __global__ void __launch_bounds__(1 << (NB - 4), NB <= 12 ? 3 : 1)
-fwht_rows_reg_kernel(const double2* __restrict__ B, double2* __restrict__ C, double* __restrict__ sq,
+fwht_rows_reg_kernel(const double2* __restrict__ A, double2* __restrict__ C, double* __restrict__ sq,
                      const double* __restrict__ thrf2, uint64_t cap, unsigned long long* __restrict__ count,
                      uint64_t* __restrict__ idx) {
   static_assert(NB >= 9 && NB <= 13, "register FWHT rows: 9 <= n <= 13");
@@ -210,9 +178,11 @@ fwht_rows_reg_kernel(const double2* __restrict__ B, double2* __restrict__ C, dou
   extern __shared__ double2 rows_smem[];
   const uint32_t t = threadIdx.x, m0 = blockIdx.x;  // one row per CTA (a persistent variant with
   double2 v[RG];                                     // an L2 prefetch of the next row measured slower)
-  const double2* row = B + size_t(m0) * N;
 #pragma unroll
-  for (int r = 0; r < RG; ++r) v[r] = __ldcs(row + rows_idx<NB>(t, uint32_t(r), NB - 4));
+  for (int r = 0; r < RG; ++r) {
+    const uint32_t k = rows_idx<NB>(t, uint32_t(r), NB - 4);
+    v[r] = __ldcg(A + size_t(k) * N + (k ^ m0));
+  }
 #pragma unroll
   for (int g = 0; g < NPASS; ++g) {
     const int b = NB - 4 * (g + 1) > 0 ? NB - 4 * (g + 1) : 0;  // register window [b, b + 4)

@@ -4,6 +4,7 @@
 // (declared in include/dvqls.h).  Context-free: allocates its own device buffers per call.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <string>
 
 #include "../../include/dvqls.h"
@@ -15,7 +16,6 @@ using namespace dvqls;
 namespace {
 struct DecompBufs {
   double2* A = nullptr;
-  double2* B = nullptr;
   double2* C = nullptr;
   double* sq = nullptr;
   double* norm = nullptr;
@@ -28,7 +28,7 @@ struct DecompBufs {
   char* os = nullptr;
   cudaStream_t st = nullptr;
   ~DecompBufs() {
-    cudaFree(A); cudaFree(B); cudaFree(C); cudaFree(sq); cudaFree(norm); cudaFree(count); cudaFree(idx); cudaFree(oc); cudaFree(os);
+    cudaFree(A); cudaFree(C); cudaFree(sq); cudaFree(norm); cudaFree(count); cudaFree(idx); cudaFree(oc); cudaFree(os);
     cudaFree(thr0); cudaFree(fro); cudaFree(outL);
     if (st) cudaStreamDestroy(st);
   }
@@ -40,15 +40,15 @@ int decomp_fail(int code, const char* msg) {
   return code;
 }
 
-// NEXT-4 device pass over B (XOR diagonals of A as rows; n < 5: straight from A).
-// MODE 0: all coefficients into C;  MODE 1: candidates + per-row |c|^2 (decomp.cuh).
+// NEXT-4 device pass over the XOR diagonals of A (decomp.cuh).
+// MODE 0: all coefficients into C;  MODE 1: candidates + per-row |c|^2.
 template <int NB, int MODE>
 int launch_rows_reg(DecompBufs& b, uint64_t cap) {
   const void* fn = (const void*)&decomp::fwht_rows_reg_kernel<NB, MODE>;
   const int smem = int(sizeof(double2) << NB);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
     return decomp_fail(DVQLS_E_CUDA, "fwht_rows_reg_kernel smem");
-  decomp::fwht_rows_reg_kernel<NB, MODE><<<1u << NB, 1u << (NB - 4), smem, b.st>>>(b.B, b.C, b.sq, b.thr0, cap,
+  decomp::fwht_rows_reg_kernel<NB, MODE><<<1u << NB, 1u << (NB - 4), smem, b.st>>>(b.A, b.C, b.sq, b.thr0, cap,
                                                                                   b.count, b.idx);
   return DVQLS_OK;
 }
@@ -63,17 +63,17 @@ int launch_rows(DecompBufs& b, int n, uint64_t cap) {
     default: break;
   }
   const unsigned N = 1u << n;
-  const int direct = n < 5 ? 1 : 0;
   if (cudaFuncSetAttribute((const void*)&decomp::fwht_rows_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(sizeof(double2) << n)))
     return decomp_fail(DVQLS_E_CUDA, "fwht_rows_kernel smem");
-  decomp::fwht_rows_kernel<MODE><<<N, decomp::THREADS, sizeof(double2) * N, b.st>>>(
-      direct ? b.A : b.B, n, b.C, b.sq, b.thr0, cap, b.count, b.idx, direct);
+  decomp::fwht_rows_kernel<MODE><<<N, decomp::THREADS, sizeof(double2) * N, b.st>>>(b.A, n, b.C, b.sq, b.thr0, cap,
+                                                                                  b.count, b.idx);
   return DVQLS_OK;
 }
 
-// A -> device, XOR-diagonal transposition (+ |A|^2 tile sums); write_c: every coefficient into C,
-// else: Parseval candidate bound, one candidate pass, exact norm (decomp.cuh)
+// A -> device in row chunks, |A|^2 of each chunk summed as it lands (pruning only); write_c: every
+// coefficient into C, else: Parseval candidate bound, one candidate pass over the XOR diagonals,
+// exact norm in the sort (decomp.cuh).  *ev0 is recorded after the upload.
 int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, bool write_c, double eps = 0.0,
                      cudaEvent_t* ev0 = nullptr) {
   if (device >= 0 && cudaSetDevice(device) != cudaSuccess) return decomp_fail(DVQLS_E_CUDA, "cudaSetDevice");
@@ -82,8 +82,8 @@ int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, boo
   if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10)
     return decomp_fail(DVQLS_E_CUDA, "libdvqls is built for sm_100a only");
   const size_t N = size_t(1) << n, NN = N * N;
-  // transposition CTAs (persistent over the (N/32)^2 tiles; one |A|^2 partial each)
-  const size_t nfro = n >= 5 ? std::min<size_t>((N >> 5) * (N >> 5), size_t(prop.multiProcessorCount) * 8) : 1;
+  const uint32_t fro_rows = uint32_t(std::min<size_t>(N, 8));  // rows per |A|^2 partial
+  const size_t nfro = N / fro_rows;
   const uint64_t cap = decomp::SORT_MAX;
   if (cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking) || cudaMalloc((void**)&b.A, sizeof(double2) * NN) ||
       cudaMalloc((void**)&b.C, sizeof(double2) * (write_c ? NN : size_t(cap))) ||
@@ -95,14 +95,18 @@ int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, boo
   if (!write_c && (cudaMalloc((void**)&b.idx, sizeof(uint64_t) * cap) ||
                    cudaMalloc((void**)&b.oc, sizeof(double2) * cap) || cudaMalloc((void**)&b.os, size_t(cap) * n)))
     return decomp_fail(DVQLS_E_CUDA, "cudaMalloc failed (pruning)");
-  if (cudaMemcpyAsync(b.A, A_host, sizeof(double2) * NN, cudaMemcpyHostToDevice, b.st))
-    return decomp_fail(DVQLS_E_CUDA, "copy of A failed");
-  if (n >= 5 && cudaMalloc((void**)&b.B, sizeof(double2) * NN)) return decomp_fail(DVQLS_E_CUDA, "cudaMalloc B");
+  // upload in chunks of ~32 MB of whole row blocks; after each chunk its |A|^2 partials
+  const size_t chunk_rows = std::max<size_t>(fro_rows, ((size_t(32) << 20) / (16 * N)) / fro_rows * fro_rows);
+  const double2* Ah = reinterpret_cast<const double2*>(A_host);
+  for (size_t r0 = 0; r0 < N; r0 += chunk_rows) {
+    const size_t rows = std::min(chunk_rows, N - r0);
+    if (cudaMemcpyAsync(b.A + r0 * N, Ah + r0 * N, sizeof(double2) * rows * N, cudaMemcpyHostToDevice, b.st))
+      return decomp_fail(DVQLS_E_CUDA, "copy of A failed");
+    if (!write_c)
+      decomp::fro_rows_kernel<<<unsigned(rows / fro_rows), 256, 0, b.st>>>(b.A, uint32_t(N), uint32_t(r0), fro_rows,
+                                                                           b.fro);
+  }
   if (ev0 && (cudaEventCreate(ev0) || cudaEventRecord(*ev0, b.st))) return decomp_fail(DVQLS_E_CUDA, "event");
-  if (n >= 5)
-    decomp::xor_transpose_kernel<<<unsigned(nfro), 256, 0, b.st>>>(b.A, n, b.B, b.fro);  // persistent
-  else
-    decomp::fro_small_kernel<<<1, 256, 0, b.st>>>(b.A, uint32_t(NN), b.fro);
   int rc;
   if (write_c) {
     rc = launch_rows<0>(b, n, 0);
