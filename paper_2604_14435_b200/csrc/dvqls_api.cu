@@ -572,8 +572,8 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
     fail(ctx, DVQLS_E_ARG, "prefix must be 0 or 1");
     return bail(DVQLS_E_ARG);
   }
-  if (o.variant < 0 || o.variant > 3) {
-    fail(ctx, DVQLS_E_ARG, "variant must be 0..3");
+  if (o.variant < 0 || o.variant > 4) {
+    fail(ctx, DVQLS_E_ARG, "variant must be 0..4");
     return bail(DVQLS_E_ARG);
   }
   if (o.allreduce != DVQLS_ALLREDUCE_P2P && o.allreduce != DVQLS_ALLREDUCE_NCCL) {
@@ -684,7 +684,7 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
     ctx->kc = stream_hh_cfg(n);
   } else if (n <= 12) {
     ctx->path = Path::onchip;
-    ctx->kc = onchip_cfg(n);
+    ctx->kc = onchip_cfg(n, o.variant == 4);
   } else {
     ctx->path = Path::pstream;
     // n >= 16 (scratch no longer L2-resident): TMA bulk-copy staging of the last-pass and large-run

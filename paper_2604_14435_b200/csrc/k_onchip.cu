@@ -7,14 +7,20 @@
 
 namespace dvqls {
 
-KernelCfg onchip_cfg(int n) {
+template <int NQ, bool XS>
+static KernelCfg cfg_of() {
   KernelCfg k;
-  if (n != 11 && n != 12) return k;
-  k.fn = n == 11 ? (const void*)&onchip::onchip_plane_kernel<11> : (const void*)&onchip::onchip_plane_kernel<12>;
-  k.warps = onchip::WARPS;
-  k.groups = n == 11 ? onchip::Sh<11>::NG : onchip::Sh<12>::NG;
-  k.smem = n == 11 ? onchip::smem_bytes<11>() : onchip::smem_bytes<12>();
+  k.fn = (const void*)&onchip::onchip_plane_kernel<NQ, XS>;
+  k.warps = onchip::Sh<NQ, XS>::W;
+  k.groups = onchip::Sh<NQ, XS>::NG;
+  k.smem = onchip::smem_bytes<NQ, XS>();
   return k;
+}
+
+KernelCfg onchip_cfg(int n, bool x_in_smem) {
+  if (n == 11) return x_in_smem ? cfg_of<11, true>() : cfg_of<11, false>();
+  if (n == 12) return x_in_smem ? cfg_of<12, true>() : cfg_of<12, false>();
+  return KernelCfg{};
 }
 
 void launch_to_planar4(const double2* x, uint32_t N, uint32_t K, double* xq, cudaStream_t st) {

@@ -31,7 +31,7 @@ PrefixCfg prefix_cfg(int n, int layers, bool cluster = true);
 void launch_finalize(const double* ep, int K, int n, double* out, cudaStream_t st);
 
 // ---- k_onchip.cu: n = 11, 12 uniform b (onchip_plane.cuh) + its planar copy of x
-KernelCfg onchip_cfg(int n);
+KernelCfg onchip_cfg(int n, bool x_in_smem = false);
 void launch_to_planar4(const double2* x, uint32_t N, uint32_t K, double* xq, cudaStream_t st);
 
 // ---- k_stream_c.cu: complex streaming kernels for Householder U_b, n = 11..24 (stream.cuh):

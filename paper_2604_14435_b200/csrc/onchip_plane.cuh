@@ -44,19 +44,25 @@ __device__ __forceinline__ double ldx(const double* base, uint32_t byte_off) {
   return __ldg(reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(base) ^ uintptr_t(byte_off)));
 }
 
-template <int NQ>
+// XS: the x planes [x_re | x_im] staged in SMEM per theta (signs by LOP3 instead of the -x copies);
+// fewer groups then fit (n = 11: 10 warps, n = 12: 8 warps)
+template <int NQ, bool XS>
+constexpr int warps_of() { return XS ? (NQ == 11 ? 10 : 8) : WARPS; }
+
+template <int NQ, bool XS = false>
 struct Sh {
+  static constexpr int W = warps_of<NQ, XS>();
   static constexpr int TB = NQ - RB;          // thread bits per plane group
   static constexpr int GT = 1 << TB;          // threads per group (32 or 64)
   static constexpr int N = 1 << NQ;
-  static constexpr int NG = WARPS * 32 / GT;  // groups per CTA
+  static constexpr int NG = W * 32 / GT;      // groups per CTA
   static constexpr uint32_t BUFB = uint32_t(N + N / 64) * 8u;  // padded exchange buffer bytes
 };
 __host__ __device__ constexpr uint32_t pslot(uint32_t i) { return i + (i >> 6); }
 
-template <int NQ>
+template <int NQ, bool XS = false>
 __host__ __device__ constexpr size_t smem_bytes() {
-  return size_t(Sh<NQ>::NG) * (Sh<NQ>::BUFB + 4 * 8 + 2 * 8);
+  return size_t(Sh<NQ, XS>::NG) * (Sh<NQ, XS>::BUFB + 4 * 8 + 2 * 8) + (XS ? sizeof(double) * 2 * (size_t(1) << NQ) : 0);
 }
 
 // xq[K][4][N] = [x_re | -x_re | x_im | -x_im] per theta
@@ -132,6 +138,45 @@ __device__ __forceinline__ void gather(double (&v)[R], const double* xt, uint32_
   }
 }
 
+// XS: the same walks over the SMEM planes [x_re | x_im] at shared-window address xs; the Pauli
+// sign of register r is sg0 ^ parity(r & zh), toggled along the Gray code, applied by flip()
+template <int NQ>
+__device__ __forceinline__ void gather_s(double (&v)[R], uint32_t xs, uint32_t pl, uint32_t mh, uint32_t tl,
+                                         uint32_t zh, uint32_t sg0) {
+  using S = Sh<NQ>;
+  uint32_t a = xs + ((pl << NQ) | (mh << S::TB) | tl) * 8u;
+  uint32_t sg = sg0 << 31;
+#pragma unroll
+  for (int kk = 0; kk < R; ++kk) {
+    const int r = kk ^ (kk >> 1);
+    if (kk) {
+      const int bb = ctz_c(kk);
+      a ^= (1u << (S::TB + bb)) * 8u;
+      sg ^= ((zh >> bb) & 1u) << 31;
+    }
+    v[r] = flip(lds(a), sg);
+  }
+}
+template <int NQ>
+__device__ __forceinline__ double readout_s(const double (&v)[R], uint32_t xs, uint32_t rp, uint32_t mh, uint32_t tl,
+                                            uint32_t zh, uint32_t sg0) {
+  using S = Sh<NQ>;
+  uint32_t a = xs + ((rp << NQ) | (mh << S::TB) | tl) * 8u;
+  uint32_t sg = sg0 << 31;
+  double ac[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int kk = 0; kk < R; ++kk) {
+    const int r = kk ^ (kk >> 1);
+    if (kk) {
+      const int bb = ctz_c(kk);
+      a ^= (1u << (S::TB + bb)) * 8u;
+      sg ^= ((zh >> bb) & 1u) << 31;
+    }
+    ac[kk & 3] = fma(flip(lds(a), sg), v[r], ac[kk & 3]);
+  }
+  return (ac[0] + ac[1]) + (ac[2] + ac[3]);
+}
+
 template <int NQ>
 __device__ __forceinline__ double readout(const double (&v)[R], const double* xt, uint32_t rp, uint32_t mh,
                                           uint32_t tl, uint32_t zh, uint32_t sg0) {
@@ -150,18 +195,20 @@ __device__ __forceinline__ double readout(const double (&v)[R], const double* xt
   return (ac[0] + ac[1]) + (ac[2] + ac[3]);
 }
 
-template <int NQ>
-__global__ void __launch_bounds__(WARPS * 32, 1)  // <= 168 registers: 12 warps per SM
+template <int NQ, bool XS = false>
+__global__ void __launch_bounds__(warps_of<NQ, XS>() * 32, 1)  // <= 168 registers
 onchip_plane_kernel(const double* __restrict__ xq_all, const PauliTerm* __restrict__ tab,
                     const double2* __restrict__ coef, int L, int64_t c0, int64_t C, int K,
                     double* __restrict__ out_terms, double* __restrict__ partials, int with_cost,
                     double* __restrict__ red_out, unsigned* __restrict__ counter, P2PArgs p2p) {
-  using S = Sh<NQ>;
+  using S = Sh<NQ, XS>;
   constexpr int TB = S::TB, GT = S::GT, N = S::N, NG = S::NG;
-  // SMEM: NG padded exchange buffers | acc[NG][4] | half[NG][2] (cross-warp readout sums)
+  // SMEM: NG padded exchange buffers | acc[NG][4] | half[NG][2] (cross-warp readout sums) | XS: [x_re | x_im]
   const uint32_t sb = sbase();
   double* sacc = reinterpret_cast<double*>(reinterpret_cast<char*>(dvqls_smem) + size_t(NG) * S::BUFB);
   double* shalf = sacc + 4 * NG;
+  double* sx = shalf + 2 * NG;  // 16-byte aligned: NG * (BUFB + 48) is a multiple of 16
+  const uint32_t xs = sb + uint32_t(size_t(NG) * (S::BUFB + 48));
   const int group = int(threadIdx.x) / GT;
   const uint32_t t = threadIdx.x % GT;
   const uint32_t buf = sb + uint32_t(group) * S::BUFB;
@@ -188,7 +235,11 @@ onchip_plane_kernel(const double* __restrict__ xq_all, const PauliTerm* __restri
     const int64_t pa = max(Fb, int64_t(kth) * C) - int64_t(kth) * C;
     const int64_t pb = min(Fe, int64_t(kth + 1) * C) - int64_t(kth) * C;
     const double* xt = xq_all + size_t(kth) * 4 * N;
-    __syncthreads();  // previous phase's accumulators have been summed
+    __syncthreads();  // previous phase's accumulators have been summed (and its x reads done)
+    if (XS) {  // stage [x_re | x_im] (planes 0 and 2 of the planar copy)
+      for (int i = threadIdx.x; i < 2 * N; i += blockDim.x) sx[i] = xt[i < N ? i : N + i];
+      __syncthreads();
+    }
     if (t == 0) gacc[0] = gacc[1] = gacc[2] = gacc[3] = 0.0;
     int cb, ce;
     {
@@ -224,7 +275,8 @@ onchip_plane_kernel(const double* __restrict__ xq_all, const PauliTerm* __restri
         {  // ---- a4: c-A_k on this plane (layout A)
           const uint32_t mh = Tk.xm >> TB, tl = t ^ (Tk.xm & (GT - 1)), zh = Tk.zm >> TB;
           const uint32_t sg0 = (__popc(tl & Tk.zm & (GT - 1)) ^ __popc(mh & zh)) & 1u;
-          gather<NQ>(v, xt, pl, mh, tl, zh, sg0);
+          if (XS) gather_s<NQ>(v, xs, pl, mh, tl, zh, sg0);
+          else gather<NQ>(v, xt, pl, mh, tl, zh, sg0);
         }
         if (s > 0) {
           const int p = NQ - 1 - (s - 1);  // index bit of Z_j
@@ -255,7 +307,7 @@ onchip_plane_kernel(const double* __restrict__ xq_all, const PauliTerm* __restri
           const uint32_t rp = pl ^ qi, xs = qi & (pl ^ 1u);
           const uint32_t mh = Tl.xm >> TB, tl = t ^ (Tl.xm & (GT - 1)), zh = Tl.zm >> TB;
           const uint32_t sg0 = (__popc(t & Tl.zm & (GT - 1)) & 1u) ^ xs;
-          acc += readout<NQ>(v, xt, rp, mh, tl, zh, sg0);
+          acc += XS ? readout_s<NQ>(v, xs, rp, mh, tl, zh, sg0) : readout<NQ>(v, xt, rp, mh, tl, zh, sg0);
         }
       }
 #pragma unroll
