@@ -40,7 +40,8 @@ sys.path.insert(0, ROOT)
 
 from dvqls_inputs import configs  # noqa: E402
 
-CONFIGS = {"cfg1": configs.cfg1, "cfg3": configs.cfg3, "cfg4": configs.cfg4, "cfg5": configs.cfg5}
+CONFIGS = {"cfg1": configs.cfg1, "cfg3": configs.cfg3, "cfg4": configs.cfg4, "cfg5": configs.cfg5,
+           "cfg5amp": configs.cfg5_amplitudes}
 METRIC = "Hadamard-test circuits/sec & cost evals/sec, 10q 90,112 circuits, 1/2/4/8 B200"
 L2_FLUSH_BYTES = 256 << 20
 
@@ -163,7 +164,28 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def hh_stream_bytes_per_eval(w, circuits=None):
+    """Householder streaming kernel (stream_hh_kernel, n >= 13): per numerator circuit three read-only
+    sweeps of the x gather (16N each) and of h (16N each) plus the readout's x (16N) = 112N; per
+    denominator 32N.  x and h stay L2-resident up to n ~ 21, so these are L2 bytes there."""
+    N = 1 << w.n
+    c = np.arange(w.n_circuits) if circuits is None else circuits
+    s = (c // 2) % (w.n + 1)
+    num = int(np.count_nonzero(s))
+    return num * 112 * N + (c.size - num) * 32 * N
+
+
 def streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, grid=None):
+    if w.bkind != 0:
+        b = hh_stream_bytes_per_eval(w, local_c) * KT
+        ach = b / (had_ms * 1e-3)
+        peak = float(peaks["hbm_gbs"]) * 1e9
+        return {"bound": "hbm", "kernel": "stream_hh_kernel<12>", "achieved": ach / 1e9, "peak": peak / 1e9,
+                "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                "note": (f"algorithmic bytes per launch = {b:.4g} (112N per numerator circuit: three read-only "
+                         "sweeps of x and h + the readout; 32N per denominator) / mean CUDA-event kernel time; "
+                         f"peak = hbm_gbs of {peak_src} MEASURED_PEAKS.json; x and h are L2-resident up to "
+                         "n ~ 21, so the real roof there is L2")}
     b = hbm_bytes_per_eval(w, local_c) * KT
     b96 = smem_bytes_per_eval(w, local_c) * KT
     ach = b / (had_ms * 1e-3)
@@ -316,7 +338,7 @@ def main():
     ap.add_argument("--no-next2", action="store_true", help="skip the NEXT-2 fast-path side measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    w = CONFIGS[args.config](args.n) if args.config == "cfg5" else CONFIGS[args.config]()
+    w = CONFIGS[args.config](args.n) if args.config.startswith("cfg5") else CONFIGS[args.config]()
 
     if args.impl == "reference":
         return run_reference(args, w)

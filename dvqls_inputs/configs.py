@@ -107,6 +107,16 @@ def cfg5(n: int, seed: int = 0) -> Workload:
     return Workload(f"cfg5_n{n}_L64_d3", n, 3, terms, B_UNIFORM, None, seed)
 
 
+def cfg5_amplitudes(n: int, seed: int = 0) -> Workload:
+    """Config 5's LCU and depth with a general b ("general b"): a seeded random normalised
+    complex b, U_b its Householder completion (SURVEY §8(c) reading 5)."""
+    w = cfg5(n, seed)
+    w.name = f"cfg5_amp_n{n}_L64_d3"
+    w.bkind = B_AMPLITUDES
+    w.b = seeds.random_b(n, seed + 1)
+    return w
+
+
 def random_workload(n: int, L: int, layers: int, seed: int = 0, amplitudes: bool = False,
                     entangler: int = 0) -> Workload:
     terms = seeds.random_lcu(n, L, seed)
