@@ -690,7 +690,7 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
     // n >= 16 (scratch no longer L2-resident): TMA bulk-copy staging of the last-pass and large-run
     // mid-pass tiles (measured +1-3 % at n = 16..20, -5 % at n = 14 where the scratch stays in L2)
     const int stage_from = o.stage == 1 ? 13 : 16;
-    ctx->kc = stream_plane_cfg(o.stage != -1 && n >= stage_from, o.variant == 3 ? 2 : 3);
+    ctx->kc = stream_plane_cfg(o.stage != -1 && n >= stage_from);
   }
   if (!ctx->kc.fn) {
     fail(ctx, DVQLS_E_UNSUPPORTED, "no Hadamard-test kernel for n = %d", n);

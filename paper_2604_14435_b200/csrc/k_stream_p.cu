@@ -8,14 +8,10 @@
 
 namespace dvqls {
 
-KernelCfg stream_plane_cfg(bool staged, int minb) {
+KernelCfg stream_plane_cfg(bool staged) {
   KernelCfg k;
-  if (minb == 2)
-    k.fn = staged ? (const void*)&streamp::stream_plane_kernel<12, true, 2>
-                  : (const void*)&streamp::stream_plane_kernel<12, false, 2>;
-  else
-    k.fn = staged ? (const void*)&streamp::stream_plane_kernel<12, true, 3>
-                  : (const void*)&streamp::stream_plane_kernel<12, false, 3>;
+  k.fn = staged ? (const void*)&streamp::stream_plane_kernel<12, true>
+                : (const void*)&streamp::stream_plane_kernel<12, false>;
   k.warps = stream::TS<12>::THREADS / 32;
   k.groups = 1;
   k.smem = staged ? streamp::staged_smem<12>() : streamp::tile_smem<12>();

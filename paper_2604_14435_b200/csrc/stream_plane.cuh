@@ -381,9 +381,12 @@ __device__ __forceinline__ double last_pass(const double* __restrict__ phi, cons
 
 // a3-a9 for n >= 11, uniform b: one circuit per CTA at a time, Re plane then Im plane.
 // x_all: planar thetas [K][re 2^n | im 2^n];  scratch: 2^n doubles per CTA (n > TB).
-// MINB: CTAs per SM the register budget is sized for (3: 80 registers, with spills; 2: up to 128)
-template <int TB, bool STAGED = false, int MINB = 3>
-__global__ void __launch_bounds__(TS<TB>::THREADS, MINB)
+// 3 CTAs per SM (80 registers; ptxas spills ~120-180 B): measured faster than 2 CTAs per SM with
+// 112 registers and no spills (n = 18: 1237 vs 1299 ms, n = 20: 6144 vs 6300 ms per K = 2 step;
+// profiles/r2_cfg5/minb_*.json)
+constexpr int MIN_CTAS = 3;
+template <int TB, bool STAGED = false>
+__global__ void __launch_bounds__(TS<TB>::THREADS, MIN_CTAS)
 stream_plane_kernel(const double* __restrict__ x_all, const PauliTerm* __restrict__ tab,
                     const double2* __restrict__ coef, int L, int n, int64_t c0, int64_t C,
                     const int64_t* __restrict__ cidx, double* __restrict__ scratch, double* __restrict__ out_terms,
