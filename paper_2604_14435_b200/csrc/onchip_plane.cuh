@@ -144,7 +144,8 @@ template <int NQ>
 __device__ __forceinline__ void gather_s(double (&v)[R], uint32_t xs, uint32_t pl, uint32_t mh, uint32_t tl,
                                          uint32_t zh, uint32_t sg0) {
   using S = Sh<NQ>;
-  uint32_t a = xs + ((pl << NQ) | (mh << S::TB) | tl) * 8u;
+  // (xs is not aligned to the plane size: the Gray-code chain runs on the offset, added to xs)
+  uint32_t a = ((pl << NQ) | (mh << S::TB) | tl) * 8u;
   uint32_t sg = sg0 << 31;
 #pragma unroll
   for (int kk = 0; kk < R; ++kk) {
@@ -154,14 +155,14 @@ __device__ __forceinline__ void gather_s(double (&v)[R], uint32_t xs, uint32_t p
       a ^= (1u << (S::TB + bb)) * 8u;
       sg ^= ((zh >> bb) & 1u) << 31;
     }
-    v[r] = flip(lds(a), sg);
+    v[r] = flip(lds(xs + a), sg);
   }
 }
 template <int NQ>
 __device__ __forceinline__ double readout_s(const double (&v)[R], uint32_t xs, uint32_t rp, uint32_t mh, uint32_t tl,
                                             uint32_t zh, uint32_t sg0) {
   using S = Sh<NQ>;
-  uint32_t a = xs + ((rp << NQ) | (mh << S::TB) | tl) * 8u;
+  uint32_t a = ((rp << NQ) | (mh << S::TB) | tl) * 8u;
   uint32_t sg = sg0 << 31;
   double ac[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -172,7 +173,7 @@ __device__ __forceinline__ double readout_s(const double (&v)[R], uint32_t xs, u
       a ^= (1u << (S::TB + bb)) * 8u;
       sg ^= ((zh >> bb) & 1u) << 31;
     }
-    ac[kk & 3] = fma(flip(lds(a), sg), v[r], ac[kk & 3]);
+    ac[kk & 3] = fma(flip(lds(xs + a), sg), v[r], ac[kk & 3]);
   }
   return (ac[0] + ac[1]) + (ac[2] + ac[3]);
 }
