@@ -305,9 +305,9 @@ onchip_plane_kernel(const double* __restrict__ xq_all, const PauliTerm* __restri
           fwht<0, RB>(v);
         }
         {  // ---- a8: c-A_l + this plane's readout half (Re S: own plane; Im S: the other one)
-          const uint32_t rp = pl ^ qi, xs = qi & (pl ^ 1u);
+          const uint32_t rp = pl ^ qi, xsg = qi & (pl ^ 1u);
           const uint32_t mh = Tl.xm >> TB, tl = t ^ (Tl.xm & (GT - 1)), zh = Tl.zm >> TB;
-          const uint32_t sg0 = (__popc(t & Tl.zm & (GT - 1)) & 1u) ^ xs;
+          const uint32_t sg0 = (__popc(t & Tl.zm & (GT - 1)) & 1u) ^ xsg;
           acc += XS ? readout_s<NQ>(v, xs, rp, mh, tl, zh, sg0) : readout<NQ>(v, xt, rp, mh, tl, zh, sg0);
         }
       }
