@@ -180,12 +180,14 @@ def streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, grid=None):
         b = hh_stream_bytes_per_eval(w, local_c) * KT
         ach = b / (had_ms * 1e-3)
         peak = float(peaks["hbm_gbs"]) * 1e9
-        return {"bound": "hbm", "kernel": "stream_hh_kernel<12>", "achieved": ach / 1e9, "peak": peak / 1e9,
-                "unit": "GB/s", "frac": ach / peak, "traffic": None,
+        in_l2 = KT * 16 * (1 << w.n) + 16 * (1 << w.n) <= 100 << 20  # x of every theta + h
+        return {"bound": "l2" if in_l2 else "hbm", "kernel": "stream_hh_kernel<12>", "achieved": ach / 1e9,
+                "peak": None if in_l2 else peak / 1e9, "unit": "GB/s", "frac": None if in_l2 else ach / peak,
+                "traffic": None,
                 "note": (f"algorithmic bytes per launch = {b:.4g} (112N per numerator circuit: three read-only "
                          "sweeps of x and h + the readout; 32N per denominator) / mean CUDA-event kernel time; "
-                         f"peak = hbm_gbs of {peak_src} MEASURED_PEAKS.json; x and h are L2-resident up to "
-                         "n ~ 21, so the real roof there is L2")}
+                         + ("x and h are L2-resident here and MEASURED_PEAKS.json has no L2 figure, so no fraction"
+                            if in_l2 else f"peak = hbm_gbs of {peak_src} MEASURED_PEAKS.json"))}
     b = hbm_bytes_per_eval(w, local_c) * KT
     b96 = smem_bytes_per_eval(w, local_c) * KT
     ach = b / (had_ms * 1e-3)

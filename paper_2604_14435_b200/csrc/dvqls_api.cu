@@ -572,8 +572,8 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
     fail(ctx, DVQLS_E_ARG, "prefix must be 0 or 1");
     return bail(DVQLS_E_ARG);
   }
-  if (o.variant < 0 || o.variant > 4) {
-    fail(ctx, DVQLS_E_ARG, "variant must be 0..4");
+  if (o.variant < 0 || o.variant > 2) {
+    fail(ctx, DVQLS_E_ARG, "variant must be 0, 1 or 2");
     return bail(DVQLS_E_ARG);
   }
   if (o.allreduce != DVQLS_ALLREDUCE_P2P && o.allreduce != DVQLS_ALLREDUCE_NCCL) {
@@ -684,7 +684,9 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
     ctx->kc = stream_hh_cfg(n);
   } else if (n <= 12) {
     ctx->path = Path::onchip;
-    ctx->kc = onchip_cfg(n, o.variant == 4);
+    // n = 12: x staged in SMEM (measured 5.86e7 vs 5.00e7 circuits/s at cfg5, K=2); n = 11: x from L2
+    // (10 warps with x in SMEM measured no faster: profiles/r2_onchip/)
+    ctx->kc = onchip_cfg(n, n == 12);
   } else {
     ctx->path = Path::pstream;
     // n >= 16 (scratch no longer L2-resident): TMA bulk-copy staging of the last-pass and large-run

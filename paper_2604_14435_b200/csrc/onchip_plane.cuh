@@ -45,7 +45,9 @@ __device__ __forceinline__ double ldx(const double* base, uint32_t byte_off) {
 }
 
 // XS: the x planes [x_re | x_im] staged in SMEM per theta (signs by LOP3 instead of the -x copies);
-// fewer groups then fit (n = 11: 10 warps, n = 12: 8 warps)
+// fewer groups then fit (n = 11: 10 warps, n = 12: 8 warps).  Default for n = 12, where the x
+// reads from L2 (128 KB per theta, no room in L1) stalled the 12-warp kernel: 0.60 vs 0.51 of the
+// FP64 pipe at cfg5 n = 12 (profiles/r2_onchip/); n = 11 keeps x in L2 (32 KB, 10 warps no faster).
 template <int NQ, bool XS>
 constexpr int warps_of() { return XS ? (NQ == 11 ? 10 : 8) : WARPS; }
 

@@ -227,21 +227,3 @@ def test_cfg5_largest_sizes_sampled(dv, n):
     ref = sim.workload_terms(w, th, idx=idx)
     assert np.min(np.abs(ref)) >= 1e-5
     assert np.max(np.abs(g - ref)) <= TOL
-
-
-@pytest.mark.parametrize("n,L,ent", [(11, 3, 0), (12, 2, 1)])
-def test_onchip_x_in_smem_variant(dv, n, L, ent):
-    """n = 11, 12 with the x planes staged in SMEM (opts.variant = 4; signs by LOP3): every term
-    and a K = 3 batch vs the oracle, terms bitwise equal to the default on-chip kernel."""
-    w = configs.random_workload(n, L, 2, seed=120 + n, entangler=ent)
-    th = w.theta0()
-    a = dv.from_workload(w, variant=4, max_batch=3)
-    b = dv.from_workload(w, max_batch=3)
-    try:
-        ta, tb = a.terms(th), b.terms(th)
-        _check_batch(a, w, np.stack([w.theta0(s) for s in (1, 2, 3)]))
-    finally:
-        a.destroy()
-        b.destroy()
-    assert np.array_equal(ta, tb)
-    assert np.max(np.abs(ta - sim.workload_terms(w, th))) <= TOL
