@@ -381,7 +381,7 @@ def main():
     def make_ctx(timing, nccl_id):
         # device memory comes from torch: the library carves its tables from this workspace
         ws_bytes = dvqls.workspace_size(w.n, w.layers, w.L, device=local, rank=rank, world=world,
-                                        max_batch=max(KT, 1), **{k: v for k, v in vopts.items() if k not in ("graphs", "variant")})
+                                        max_batch=max(KT, 1), **vopts)
         workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         return dvqls.Context(w.n, w.layers, chars, co, w.bkind, w.b, device=local, rank=rank, world=world,
                              nccl_id=nccl_id, entangler=w.entangler, stream=stream, timing=timing,

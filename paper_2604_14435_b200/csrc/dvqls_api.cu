@@ -572,8 +572,8 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
     fail(ctx, DVQLS_E_ARG, "prefix must be 0 or 1");
     return bail(DVQLS_E_ARG);
   }
-  if (o.variant < 0 || o.variant > 4) {
-    fail(ctx, DVQLS_E_ARG, "variant must be 0..4");
+  if (o.variant < 0 || o.variant > 2) {
+    fail(ctx, DVQLS_E_ARG, "variant must be 0, 1 or 2");
     return bail(DVQLS_E_ARG);
   }
   if (o.allreduce != DVQLS_ALLREDUCE_P2P && o.allreduce != DVQLS_ALLREDUCE_NCCL) {
@@ -692,8 +692,7 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
     // n >= 16 (scratch no longer L2-resident): TMA bulk-copy staging of the last-pass and large-run
     // mid-pass tiles (measured +1-3 % at n = 16..20, -5 % at n = 14 where the scratch stays in L2)
     const int stage_from = o.stage == 1 ? 13 : 16;
-    ctx->kc = o.variant == 3 ? stream_plane_cfg(o.stage != -1 && n >= stage_from)
-                             : stream64_cfg(o.variant == 4 ? 6 : 4);
+    ctx->kc = stream_plane_cfg(o.stage != -1 && n >= stage_from);
   }
   if (!ctx->kc.fn) {
     fail(ctx, DVQLS_E_UNSUPPORTED, "no Hadamard-test kernel for n = %d", n);

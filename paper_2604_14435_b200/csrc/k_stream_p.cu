@@ -3,7 +3,6 @@
 #include <algorithm>
 
 #include "launch.h"
-#include "stream64.cuh"
 #include "stream_plane.cuh"
 #include "tile.cuh"
 
@@ -16,15 +15,6 @@ KernelCfg stream_plane_cfg(bool staged) {
   k.warps = stream::TS<12>::THREADS / 32;
   k.groups = 1;
   k.smem = staged ? streamp::staged_smem<12>() : streamp::tile_smem<12>();
-  return k;
-}
-
-KernelCfg stream64_cfg(int minb) {
-  KernelCfg k;
-  k.fn = minb == 6 ? (const void*)&s64::stream64_kernel<6> : (const void*)&s64::stream64_kernel<4>;
-  k.warps = s64::NT / 32;
-  k.groups = 1;
-  k.smem = s64::smem_bytes();
   return k;
 }
 

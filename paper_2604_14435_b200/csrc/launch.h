@@ -41,7 +41,6 @@ KernelCfg stream_hh_cfg(int n);
 
 // ---- k_stream_p.cu: n >= 13 uniform b (stream_plane.cuh), global-memory prefix (tile.cuh)
 KernelCfg stream_plane_cfg(bool staged);
-KernelCfg stream64_cfg(int min_ctas = 4);  // 64 doubles per thread, transposed scratch tiles (stream64.cuh)
 void launch_to_planar(const double2* x, uint32_t N, uint32_t K, double* xp, cudaStream_t st);
 // V(theta_k)|0> for k < K in global memory (x: K x 2^n), ping-pong buffer x2 (2^n), gate table
 // gates (2 n layers); returns a cudaError_t
