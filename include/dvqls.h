@@ -268,8 +268,9 @@ int dvqls_terms_subset(dvqls_ctx* ctx, const double* theta, const int64_t* idx, 
  * The output feeds dvqls_create (pauli_terms, coeffs) directly.  Synchronous; allocates its
  * own device buffers (16 * 4^n bytes for A, plus the candidates).  One pass over the XOR
  * diagonals of A: candidates above eps * ||A||_F / 2^{n/2} * (1 - 1e-9) (Parseval) are kept, then
- * filtered with the exact ||c||_2 = sqrt(sum |c|^2).  More than 4096 candidates:
- * DVQLS_E_UNSUPPORTED (*out_L = count).
+ * filtered with the exact ||c||_2 = sqrt(sum |c|^2) and ordered in one CTA (<= 4096 candidates)
+ * or, beyond that, by a second candidate pass into buffers of the counted size and a global
+ * bitonic sort (same order).
  * Errors: dvqls_decompose_error(). */
 int dvqls_decompose(int n, const double* A, double eps, int64_t max_terms, char* out_paulis,
                     double* out_coeffs, int64_t* out_L, double* out_norm, int device, float* out_ms);

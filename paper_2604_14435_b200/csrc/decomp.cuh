@@ -311,5 +311,78 @@ sort_emit_kernel(const double2* __restrict__ C, int n, const uint64_t* __restric
   }
 }
 
+// ---- more than SORT_MAX candidates: the same order with a global bitonic sort --------------
+// ||c||_2 = sqrt(sum_m sq[m]) in the fixed order of sort_emit_kernel (one CTA of THREADS)
+__global__ void __launch_bounds__(THREADS) norm_kernel(const double* __restrict__ sq, int n, double* __restrict__ norm) {
+  __shared__ double red[THREADS];
+  double a = 0.0;
+  for (uint32_t i = threadIdx.x; i < (1u << n); i += THREADS) a += sq[i];
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int off = THREADS / 2; off >= 1; off >>= 1) {
+    if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *norm = sqrt(red[0]);
+}
+
+// sort keys of the L candidates, padded to P (a power of two): kept ones (|c| >= max(1e-14,
+// eps ||c||_2)) get (~round(|c| / (1e-12 ||c||_2)), lex code), the rest sort last; *kept counts them
+__global__ void keys_kernel(const double2* __restrict__ C, const uint64_t* __restrict__ idx, uint64_t L, uint64_t P,
+                            int n, const double* __restrict__ norm, double eps, uint64_t* __restrict__ kq,
+                            uint64_t* __restrict__ kl, uint32_t* __restrict__ ki, unsigned long long* __restrict__ kept) {
+  const double nrm = *norm, q = 1e-12 * nrm, thr = fmax(1e-14, eps * nrm);
+  const uint32_t N = 1u << n;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < P; i += uint64_t(gridDim.x) * blockDim.x) {
+    const double2 c = i < L ? C[i] : make_double2(0.0, 0.0);
+    const double a = sqrt(fma(c.x, c.x, c.y * c.y));
+    if (i < L && a >= thr) {
+      const uint64_t id = idx[i];
+      kq[i] = ~uint64_t(llround(a / q));
+      kl[i] = lex_code(uint32_t(id / N), uint32_t(id % N), n);
+      ki[i] = uint32_t(i);
+      atomicAdd(kept, 1ull);
+    } else {
+      kq[i] = ~0ull; kl[i] = ~0ull; ki[i] = 0xffffffffu;
+    }
+  }
+}
+
+// one (k, j) step of the bitonic network over P keys (ascending (kq, kl))
+__global__ void bitonic_step_kernel(uint64_t* __restrict__ kq, uint64_t* __restrict__ kl, uint32_t* __restrict__ ki,
+                                    uint64_t P, uint64_t k, uint64_t j) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < P; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t l = i ^ j;
+    if (l > i) {
+      const bool up = (i & k) == 0;
+      const bool gt = kq[i] > kq[l] || (kq[i] == kq[l] && kl[i] > kl[l]);
+      if (gt == up) {
+        uint64_t t = kq[i]; kq[i] = kq[l]; kq[l] = t;
+        t = kl[i]; kl[i] = kl[l]; kl[l] = t;
+        const uint32_t u = ki[i]; ki[i] = ki[l]; ki[l] = u;
+      }
+    }
+  }
+}
+
+// survivors in sorted order: coefficients and Pauli strings
+__global__ void emit_kernel(const double2* __restrict__ C, const uint64_t* __restrict__ idx,
+                            const uint32_t* __restrict__ ki, const unsigned long long* __restrict__ kept, int n,
+                            double2* __restrict__ out_c, char* __restrict__ out_s, unsigned long long* __restrict__ out_L) {
+  const uint64_t LK = *kept;
+  const uint32_t N = 1u << n;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *out_L = LK;
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < LK; r += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t id = idx[ki[r]];
+    out_c[r] = C[ki[r]];
+    const uint32_t m = uint32_t(id / N), z = uint32_t(id % N);
+    for (int qq = 0; qq < n; ++qq) {
+      const int b = n - 1 - qq;
+      const uint32_t xb = (m >> b) & 1u, zb = (z >> b) & 1u;
+      out_s[size_t(r) * n + qq] = xb ? (zb ? 'Y' : 'X') : (zb ? 'Z' : 'I');
+    }
+  }
+}
+
 }  // namespace decomp
 }  // namespace dvqls

@@ -943,9 +943,9 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
 }
 
 // host copy of the error word + K result rows, then the error / degeneracy checks
+// after the results (error word + K rows) were copied to h_stage + K P: checks and unpacking
 int finish_host_cost(dvqls_ctx* ctx, int K, double* out_costs, double* out_E_Psi) {
   double* h = ctx->h_stage + size_t(K) * ctx->P;
-  CK(cudaMemcpyAsync(h, ctx->d_outbuf, sizeof(double) * (1 + 5 * size_t(K)), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   unsigned word;
   std::memcpy(&word, h, sizeof word);
@@ -1109,10 +1109,18 @@ int dvqls_cost_batch(dvqls_ctx* ctx, int K, const double* thetas, double* out_co
   ctx->err.clear();
   if (K < 1 || K > ctx->max_batch) return fail(ctx, DVQLS_E_ARG, "K=%d outside [1, max_batch=%d]", K, ctx->max_batch);
   if (!thetas || !out_costs) return fail(ctx, DVQLS_E_ARG, "NULL host pointer");
+  if (int rc = check_usable(ctx)) return rc;
   const size_t tb = sizeof(double) * size_t(K) * ctx->P;
   std::memcpy(ctx->h_stage, thetas, tb);
-  CK(cudaMemcpyAsync(ctx->d_theta, ctx->h_stage, tb, cudaMemcpyHostToDevice, ctx->stream));
-  int rc = dvqls_cost_dev(ctx, K, ctx->d_theta, ctx->d_out);
+  // theta H2D from the pinned stage, the whole path, results D2H: one graph launch per call
+  double* h = ctx->h_stage + size_t(K) * ctx->P;
+  int rc = run_graph(ctx, 3, K, ctx->h_stage, h, [&] {
+    CK(cudaMemcpyAsync(ctx->d_theta, ctx->h_stage, tb, cudaMemcpyHostToDevice, ctx->stream));
+    int r = launch_eval(ctx, K, ctx->d_theta, true, ctx->d_out);
+    if (r) return r;
+    CK(cudaMemcpyAsync(h, ctx->d_outbuf, sizeof(double) * (1 + 5 * size_t(K)), cudaMemcpyDeviceToHost, ctx->stream));
+    return DVQLS_OK;
+  });
   if (rc) return rc;
   return finish_host_cost(ctx, K, out_costs, out_E_Psi);
 }

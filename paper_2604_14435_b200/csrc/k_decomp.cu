@@ -15,6 +15,10 @@ using namespace dvqls;
 // ---- NEXT-4: Pauli decomposition + pruning (decomp.cuh) ---------------------------------------
 namespace {
 struct DecompBufs {
+  uint64_t* kq = nullptr;  // global-sort keys (more than SORT_MAX candidates)
+  uint64_t* kl = nullptr;
+  uint32_t* ki = nullptr;
+  unsigned long long* kept = nullptr;
   double2* A = nullptr;
   double2* C = nullptr;
   double* sq = nullptr;
@@ -27,9 +31,10 @@ struct DecompBufs {
   double2* oc = nullptr;
   char* os = nullptr;
   cudaStream_t st = nullptr;
+  size_t nfro = 0;
   ~DecompBufs() {
     cudaFree(A); cudaFree(C); cudaFree(sq); cudaFree(norm); cudaFree(count); cudaFree(idx); cudaFree(oc); cudaFree(os);
-    cudaFree(thr0); cudaFree(fro); cudaFree(outL);
+    cudaFree(thr0); cudaFree(fro); cudaFree(outL); cudaFree(kq); cudaFree(kl); cudaFree(ki); cudaFree(kept);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -113,6 +118,7 @@ int decomp_transform(DecompBufs& b, int n, const double* A_host, int device, boo
   } else {
     decomp::prenorm_kernel<<<1, 256, 0, b.st>>>(b.fro, uint32_t(nfro), uint32_t(N), eps, b.thr0, b.count);
     rc = launch_rows<1>(b, n, cap);  // the exact norm is formed inside sort_emit_kernel
+    b.nfro = nfro;
   }
   if (rc) return rc;
   if (cudaGetLastError()) return decomp_fail(DVQLS_E_CUDA, "decomposition kernel launch failed");
@@ -160,8 +166,33 @@ int dvqls_decompose(int n, const double* A, double eps, int64_t max_terms, char*
     return decomp_fail(DVQLS_E_CUDA, "pruning failed");
   if (out_norm) *out_norm = norm;
   if (cand > decomp::SORT_MAX) {
-    *out_L = int64_t(cand);
-    return decomp_fail(DVQLS_E_UNSUPPORTED, "more than 4096 terms survive the pruning");
+    // more candidates than the one-CTA sort holds: compact them all (second candidate pass with
+    // buffers of the counted size) and sort globally (bitonic network, the same total order)
+    const size_t N = size_t(1) << n;
+    uint64_t P = 1;
+    while (P < cand) P <<= 1;
+    cudaFree(b.C); cudaFree(b.idx); cudaFree(b.oc); cudaFree(b.os);
+    b.C = nullptr; b.idx = nullptr; b.oc = nullptr; b.os = nullptr;
+    if (cudaMalloc((void**)&b.C, sizeof(double2) * cand) || cudaMalloc((void**)&b.idx, sizeof(uint64_t) * cand) ||
+        cudaMalloc((void**)&b.oc, sizeof(double2) * cand) || cudaMalloc((void**)&b.os, size_t(cand) * n) ||
+        cudaMalloc((void**)&b.kq, sizeof(uint64_t) * P) || cudaMalloc((void**)&b.kl, sizeof(uint64_t) * P) ||
+        cudaMalloc((void**)&b.ki, sizeof(uint32_t) * P) || cudaMalloc((void**)&b.kept, sizeof(unsigned long long)))
+      return decomp_fail(DVQLS_E_CUDA, "cudaMalloc failed (large candidate set)");
+    decomp::prenorm_kernel<<<1, 256, 0, b.st>>>(b.fro, uint32_t(b.nfro), uint32_t(N), eps, b.thr0, b.count);
+    if ((rc = launch_rows<1>(b, n, cand))) return rc;
+    decomp::norm_kernel<<<1, decomp::THREADS, 0, b.st>>>(b.sq, n, b.norm);
+    cudaMemsetAsync(b.kept, 0, sizeof(unsigned long long), b.st);
+    const unsigned grid = unsigned(std::min<uint64_t>(4096, (P + 255) / 256));
+    decomp::keys_kernel<<<grid, 256, 0, b.st>>>(b.C, b.idx, cand, P, n, b.norm, eps, b.kq, b.kl, b.ki, b.kept);
+    for (uint64_t k = 2; k <= P; k <<= 1)
+      for (uint64_t j = k >> 1; j > 0; j >>= 1)
+        decomp::bitonic_step_kernel<<<grid, 256, 0, b.st>>>(b.kq, b.kl, b.ki, P, k, j);
+    decomp::emit_kernel<<<grid, 256, 0, b.st>>>(b.C, b.idx, b.ki, b.kept, n, b.oc, b.os, b.outL);
+    if (out_ms && (cudaEventRecord(e1, b.st))) return decomp_fail(DVQLS_E_CUDA, "event");
+    if (cudaGetLastError() || cudaMemcpyAsync(&L, b.outL, sizeof L, cudaMemcpyDeviceToHost, b.st) ||
+        cudaMemcpyAsync(&norm, b.norm, sizeof norm, cudaMemcpyDeviceToHost, b.st) || cudaStreamSynchronize(b.st))
+      return decomp_fail(DVQLS_E_CUDA, "global sort failed");
+    if (out_norm) *out_norm = norm;
   }
   *out_L = int64_t(L);
   if (int64_t(L) > max_terms) return decomp_fail(DVQLS_E_ARG, "max_terms too small (*out_L holds the count)");

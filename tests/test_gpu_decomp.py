@@ -90,3 +90,20 @@ def test_n13_sampled(dv):
     got, norm = dv.decompose(A, 0.01)
     assert abs(norm ** 2 - np.sum(np.abs(A) ** 2) / N) <= 1e-9 * norm ** 2  # Parseval
     assert len(got) > 0 and all(abs(c) >= 0.01 * norm for c, _ in got)
+
+
+@pytest.mark.parametrize("n,eps", [(7, 0.001), (8, 0.002)])
+def test_pruned_dense_beyond_the_one_cta_sort(dv, n, eps):
+    """A dense random A keeps most of its 4^n coefficients: more than the 4,096 candidates of the
+    one-CTA sort, so the global bitonic path orders them; strings and order identical to the
+    oracle, coefficients <= 1e-12 * ||A||."""
+    rng = np.random.default_rng(700 + n)
+    N = 1 << n
+    A = rng.normal(size=(N, N)) + 1j * rng.normal(size=(N, N))
+    got, norm = dv.decompose(A, eps, max_terms=4 ** n)
+    ref, rnorm = opd.decompose_pruned(A, eps)
+    assert len(ref) > 4096
+    assert len(got) == len(ref)
+    assert [s for _, s in got] == [s for _, s in ref]
+    assert max(abs(c - r) for (c, _), (r, _) in zip(got, ref)) <= 1e-12 * np.abs(A).max()
+    assert abs(norm - rnorm) <= 1e-12 * rnorm
