@@ -6,6 +6,7 @@
 //   * shared memory: STS.128 + LDS.128 exchange   -> bytes / clk / SM
 //   * warp shuffle SHFL.BFLY (32-bit)             -> bytes / clk / SM
 //   * mixed DADD + LDS.128 (different warps)      -> do the two pipes overlap?
+//   * mixed SHFL + LDS.128 (different warps)      -> do shuffles share the shared-memory data path?
 // Cycles are read with clock64() per CTA (one CTA per SM, grid = #SMs), so the
 // numbers are per SM clock and independent of the DVFS clock during the run.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench tools/microbench.cu
@@ -143,6 +144,41 @@ __global__ void __launch_bounds__(THREADS) k_mixed(double b, int iters_d, int it
   out[blockIdx.x * THREADS + threadIdx.x] = r;
 }
 
+// half the warps do SHFL.BFLY, half do LDS.128: do shuffles and shared loads share one data path?
+__global__ void __launch_bounds__(THREADS) k_mixed_shfl(int iters_s, int iters_l, unsigned* out, long long* cyc) {
+  extern __shared__ double2 s[];
+  for (int i = threadIdx.x; i < 8192; i += THREADS) s[i] = make_double2(i, -i);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned r = 0;
+  long long t0 = clock64();
+  if (warp & 1) {
+    unsigned a0 = threadIdx.x, a1 = a0 * 3, a2 = a0 * 5, a3 = a0 * 7, a4 = a0 * 11, a5 = a0 * 13, a6 = a0 * 17, a7 = a0 * 19;
+    for (int i = 0; i < iters_s; ++i) {
+      a0 = __shfl_xor_sync(0xffffffffu, a0, 1); a1 = __shfl_xor_sync(0xffffffffu, a1, 2);
+      a2 = __shfl_xor_sync(0xffffffffu, a2, 4); a3 = __shfl_xor_sync(0xffffffffu, a3, 8);
+      a4 = __shfl_xor_sync(0xffffffffu, a4, 16); a5 = __shfl_xor_sync(0xffffffffu, a5, 3);
+      a6 = __shfl_xor_sync(0xffffffffu, a6, 5); a7 = __shfl_xor_sync(0xffffffffu, a7, 9);
+    }
+    r = a0 ^ a1 ^ a2 ^ a3 ^ a4 ^ a5 ^ a6 ^ a7;
+  } else {
+    const double2* base = s + (warp & 7) * 1024;
+    unsigned acc = 0;
+    for (int i = 0; i < iters_l; ++i) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double2 v = base[((i * 8 + q) & 31) * 32 + lane];
+        acc ^= __double2loint(v.x) ^ __double2hiint(v.x) ^ __double2loint(v.y) ^ __double2hiint(v.y);
+      }
+    }
+    r = acc;
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[blockIdx.x * THREADS + threadIdx.x] = r;
+}
+
 // dependent-chain latencies (one warp): cycles per dependent op
 __global__ void k_lat_dfma(double b, int iters, double* out, long long* cyc) {
   double a = threadIdx.x;
@@ -196,6 +232,7 @@ int main() {
   const int smem = 8192 * 16;  // 128 KB
   CK(cudaFuncSetAttribute(k_lds, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CK(cudaFuncSetAttribute(k_mixed, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CK(cudaFuncSetAttribute(k_mixed_shfl, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CK(cudaFuncSetAttribute(k_xchg, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 256 * 16));
   auto med = [&]() -> double { if (cudaMemcpy(cyc.data(), dcyc, sizeof(long long) * sms, cudaMemcpyDeviceToHost) != cudaSuccess) return -1.0; std::sort(cyc.begin(), cyc.end()); return (double)cyc[sms / 2]; };
   const int it = 4096;
@@ -223,6 +260,15 @@ int main() {
   c = med();
   const double t_d = (THREADS / 2.0) * itd * 8 / 64.0, t_l = (THREADS / 2.0) * itl * 8 * 16 / 128.0;
   printf(", \"mixed_cycles\": %.0f, \"mixed_model_sum\": %.0f, \"mixed_model_max\": %.0f", c, t_d + t_l, std::max(t_d, t_l));
+  {
+    // SHFL warps move 8 x 128 B per iteration, LDS warps 8 x 512 B: 4x the SHFL iterations for equal bytes
+    const int its = 4 * 4096, itl2 = 4096;
+    k_mixed_shfl<<<sms, THREADS, smem>>>(its, itl2, uout, dcyc); CK(cudaDeviceSynchronize());
+    c = med();
+    const double ts = (THREADS / 2.0) * its * 8 * 4 / 128.0, tl = (THREADS / 2.0) * itl2 * 8 * 16 / 128.0;
+    printf(", \"mixed_shfl_lds_cycles\": %.0f, \"mixed_shfl_lds_model_sum\": %.0f, \"mixed_shfl_lds_model_max\": %.0f", c, ts + tl,
+           std::max(ts, tl));
+  }
   {
     const int li = 1024;
     k_lat_dfma<<<1, 32>>>(1e-9, li, dout, dcyc); CK(cudaDeviceSynchronize());
