@@ -114,24 +114,22 @@ __device__ __forceinline__ double readout(const double (&v)[R], uint32_t xa, uin
   return half;
 }
 
-struct Dec {  // canonical decode of a circuit, advanced without divisions
-  int part, s, k, l;
-  __device__ __forceinline__ void next(int n1, int L) {
-    if (++part == 2) {
-      part = 0;
-      if (++s == n1) {
-        s = 0;
-        if (++k == L) { k = 0; ++l; }
-      }
-    }
-  }
-};
-
+// SMEM "small" region: per pair the task index and the Im warp's two readout halves, both double
+// buffered by iteration parity; the CTA's task counter; the per-warp partial quadruples of the
+// end-of-piece reduction
 template <int W>
 __host__ __device__ constexpr size_t small_bytes() {
-  return sizeof(double) * (size_t(W / 2) * 2 * BATCH * 2 + size_t(W / 2) * 4);
+  return sizeof(double) * (size_t(W / 2) * 4 + size_t(W) * 4) + sizeof(int) * (size_t(W / 2) * 2 + 2);
 }
 
+// a3 (within a CTA) + a9.  The CTA's share of the K x C flattened work is static and cost-weighted
+// (as in plane_kernel: it decides which thetas' x the CTA stages); inside a theta piece the six warp
+// pairs take tasks (the Re and Im circuit of one (k, l, j)) one at a time from a shared counter, so
+// no pair idles while another still holds a statically assigned tail (ncu, K = 1: SM active cycles
+// spread 6 % min-to-max under the static split).  Determinism does not depend on which pair ran a
+// task: each task's two terms go to out_terms, and after the piece the CTA sums c_l^* c_k x term
+// over the piece's circuits in a fixed order (per-thread strided loop, fixed warp tree, fixed warp
+// order) -- the weighted sums are bitwise reproducible run to run.
 __global__ void __launch_bounds__(WARPS * 32, 1)  // <= 168 registers: 12 warps per SM
 plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ tab, const double2* __restrict__ coef,
               const double2* __restrict__ hv, double hv_scale, int L, int64_t c0, int64_t C, int K,
@@ -140,8 +138,10 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
   pdl_wait();
   (void)hv; (void)hv_scale;
   constexpr size_t SMALL = small_bytes<WARPS>();
-  double* sslot = reinterpret_cast<double*>(dvqls_smem);
-  double* sacc = sslot + NP * 2 * BATCH * 2;
+  double* shalf = reinterpret_cast<double*>(dvqls_smem);  // [NP][2 parities][2 circuits]
+  double* sred = shalf + NP * 4;                            // [WARPS][4]
+  int* stask = reinterpret_cast<int*>(sred + WARPS * 4);    // [NP][2 parities]
+  int* sctr = stask + NP * 2;
   const uint32_t sb = plane::sbase();
   const uint32_t xa = (sb + uint32_t(SMALL) + XALIGN - 1) & ~(XALIGN - 1);
   {
@@ -158,8 +158,6 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
   const uint32_t buf = xa + XREG + uint32_t(warp) * BUF;
   const uint32_t baseA = buf + t * 8u, baseB = buf + t * ROW;
   const int n1 = NQ + 1;
-  double* slot = sslot + pair * (2 * BATCH * 2);
-  double* pacc = sacc + 4 * pair;
 
   const int64_t G = gridDim.x;
   const int64_t w0 = wcum(c0, NQ), Wt = wcum(c0 + C, NQ) - w0, Wall = Wt * K;
@@ -179,11 +177,14 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
   for (int k = threadIdx.x; k < K; k += blockDim.x)
     if (k < th_first || k > th_last)
       for (int q = 0; q < 4; ++q) partials[(size_t(k) * G + blockIdx.x) * 4 + q] = 0.0;
+  const int64_t tk0 = c0 >> 1;  // global task index of local task 0
 
   for (int kth = th_first; kth <= th_last; ++kth) {
     const int64_t pa = max(Fb, int64_t(kth) * C) - int64_t(kth) * C;
     const int64_t pb = min(Fe, int64_t(kth + 1) * C) - int64_t(kth) * C;
+    const int ta = int(pa >> 1), tb = int(pb >> 1);  // this piece's tasks [ta, tb)
     const double2* x = x_all + (size_t)kth * N;
+    double* terms = out_terms + (size_t)kth * C;
     __syncthreads();
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       const double2 a = x[i];
@@ -192,65 +193,32 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
       sd[2 * N + i] = a.y;
       sd[3 * N + i] = -a.y;
     }
+    if (threadIdx.x == 0) *sctr = ta;
     __syncthreads();
-    int cb, ce;
-    {
-      int64_t b, e;
-      weighted_range(c0 + pa, pb - pa, pair, NP, NQ, &b, &e);
-      cb = int(pa + (b & ~int64_t(1)));
-      ce = int(pa + (e & ~int64_t(1)));
-    }
-    if (pl == 0 && t == 0) pacc[0] = pacc[1] = pacc[2] = pacc[3] = 0.0;
-    Dec d;
-    {
-      const int64_t c = c0 + cb, tk = c >> 1, lk = tk / n1;
-      d.part = 0;
-      d.s = int(tk % n1);
-      d.k = int(lk % L);
-      d.l = int(lk / L);
-    }
 
-    // a9 (fused): pair combine every BATCH circuits (plane.cuh)
-    auto deposit = [&](int cl, double half) {
-      const int j = (cl - cb) & (BATCH - 1);
-      double* sl = slot + (((cl - cb) / BATCH) & 1) * (BATCH * 2);
-      if (t == 0) sl[2 * j + pl] = half;
-      if (j == BATCH - 1 || cl + 1 == ce) {
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + pair), "r"(64) : "memory");
-        if (pl == 0) {
-          double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
-          if (int(t) <= j) {
-            const double val = sl[2 * t] + sl[2 * t + 1];
-            const int cc = cl - j + int(t);
-            out_terms[(size_t)kth * C + cc] = val;
-            const int64_t c = c0 + cc, tk = c >> 1, lk = tk / n1;
-            const int prt = int(c & 1), ss = int(tk - lk * n1), kk = int(lk % L), ll = int(lk / L);
-            const double2 cl_ = coef[ll], ck = coef[kk];
-            const double wr = cl_.x * ck.x + cl_.y * ck.y, wi = cl_.x * ck.y - cl_.y * ck.x;
-            const double cr = (prt == 0 ? wr : -wi) * val, ci = (prt == 0 ? wi : wr) * val;
-            if (ss == 0) { e2 = cr; e3 = ci; } else { e0 = cr; e1 = ci; }
-          }
-#pragma unroll
-          for (int off = 16; off >= 1; off >>= 1) {
-            e0 += __shfl_xor_sync(0xffffffffu, e0, off);
-            e1 += __shfl_xor_sync(0xffffffffu, e1, off);
-            e2 += __shfl_xor_sync(0xffffffffu, e2, off);
-            e3 += __shfl_xor_sync(0xffffffffu, e3, off);
-          }
-          if (t == 0) { pacc[0] += e0; pacc[1] += e1; pacc[2] += e2; pacc[3] += e3; }
-        }
-      }
-    };
     // one task (Re and Im circuit) per iteration; one copy of each path (instruction-cache footprint)
+    int prev = -1;
+    double pha = 0.0, phb = 0.0;  // Re warp: its halves of the previous task
 #pragma unroll 1
-    for (int cl = cb; cl < ce; cl += 2) {
-      const Dec da = d;
-      d.next(n1, L);
-      d.next(n1, L);
-      const PauliTerm Tk = tab[da.k];
-      const PauliTerm Tl = tab[da.l];
-      if (da.s > 0) {  // numerator task: Re circuit A, Im circuit B, skewed by one phase
-        const int p = NQ - da.s;
+    for (int it = 0;; ++it) {
+      const int par = it & 1;
+      if (pl == 0 && t == 0) stask[2 * pair + par] = atomicAdd(sctr, 1);
+      // the pair's barrier: publishes the new task index and the Im warp's halves of the previous task
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + pair), "r"(64) : "memory");
+      if (pl == 0 && prev >= 0 && t < 2) {  // a9: combine the two planes' halves of the previous task
+        const double* sh = shalf + 4 * pair + 2 * (par ^ 1);
+        terms[2 * prev + int(t)] = (t == 0 ? pha : phb) + sh[t];
+      }
+      const int task = stask[2 * pair + par];
+      if (task >= tb) break;
+      const int64_t tk = tk0 + task, lk = tk / n1;
+      const int s_ = int(tk - lk * n1);
+      const int kq = int(lk % L), lq = int(lk / L);
+      const PauliTerm Tk = tab[kq];
+      const PauliTerm Tl = tab[lq];
+      double ha, hb;
+      if (s_ > 0) {  // numerator task: Re circuit A, Im circuit B, skewed by one phase
+        const int p = NQ - s_;
         double va[R], vb[R];
         gather(va, xa, pl, t, Tk);
         // seg 1: F1(A) | gather(B)
@@ -288,33 +256,64 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
         fwht<3, RB>(va);
         // seg 6: readout(A) | F4(B);  seg 7: readout(B)
         const int qa = (Tk.ny + Tl.ny) & 3, qb = (Tk.ny + Tl.ny + 3) & 3;
-        double ha = readout(va, xa, pl, t, Tl, qa);
+        ha = readout(va, xa, pl, t, Tl, qa);
         fwht<0, RB>(vb);
-        double hb = readout(vb, xa, pl, t, Tl, qb);
+        hb = readout(vb, xa, pl, t, Tl, qb);
         constexpr double sc = 1.0 / double(N);
         ha *= (qa == 1 || qa == 2) ? -sc : sc;
         hb *= (qb == 1 || qb == 2) ? -sc : sc;
-        deposit(cl, ha);
-        deposit(cl + 1, hb);
       } else {  // denominator task: c-A_k gather and c-A_l readout of each circuit
+        ha = hb = 0.0;
 #pragma unroll 1
         for (int part = 0; part < 2; ++part) {
           double v[R];
           gather(v, xa, pl, t, Tk);
           const int q = (Tk.ny + Tl.ny + 3 * part) & 3;
-          double half = readout(v, xa, pl, t, Tl, q);
-          deposit(cl + part, (q == 1 || q == 2) ? -half : half);
+          const double half = readout(v, xa, pl, t, Tl, q);
+          if (part == 0) ha = (q == 1 || q == 2) ? -half : half;
+          else hb = (q == 1 || q == 2) ? -half : half;
         }
       }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {  // fixed pair order
-      double e0 = 0, e1 = 0, e2 = 0, e3 = 0;
-      for (int g = 0; g < NP; ++g) {
-        e0 += sacc[4 * g]; e1 += sacc[4 * g + 1]; e2 += sacc[4 * g + 2]; e3 += sacc[4 * g + 3];
+      if (pl == 1 && t == 0) {
+        shalf[4 * pair + 2 * par] = ha;
+        shalf[4 * pair + 2 * par + 1] = hb;
       }
-      double* o = partials + ((size_t)kth * G + blockIdx.x) * 4;
-      o[0] = e0; o[1] = e1; o[2] = e2; o[3] = e3;
+      pha = ha;
+      phb = hb;
+      prev = task;
+    }
+    __syncthreads();  // every term of the piece is in out_terms
+    // a9: sum_c c_l^* c_k term_c over the piece [pa, pb) in a fixed order
+    {
+      double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+      for (int64_t cc = pa + threadIdx.x; cc < pb; cc += blockDim.x) {
+        const double val = terms[cc];
+        const int64_t c = c0 + cc, tk = c >> 1, lk = tk / n1;
+        const int prt = int(c & 1), ss = int(tk - lk * n1), kk = int(lk % L), ll = int(lk / L);
+        const double2 cl_ = coef[ll], ck = coef[kk];
+        const double wr = cl_.x * ck.x + cl_.y * ck.y, wi = cl_.x * ck.y - cl_.y * ck.x;
+        const double cr = (prt == 0 ? wr : -wi) * val, ci = (prt == 0 ? wi : wr) * val;
+        if (ss == 0) { e2 += cr; e3 += ci; } else { e0 += cr; e1 += ci; }
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        e0 += __shfl_xor_sync(0xffffffffu, e0, off);
+        e1 += __shfl_xor_sync(0xffffffffu, e1, off);
+        e2 += __shfl_xor_sync(0xffffffffu, e2, off);
+        e3 += __shfl_xor_sync(0xffffffffu, e3, off);
+      }
+      if (t == 0) {
+        sred[4 * warp] = e0; sred[4 * warp + 1] = e1; sred[4 * warp + 2] = e2; sred[4 * warp + 3] = e3;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {  // fixed warp order
+        double f0 = 0, f1 = 0, f2 = 0, f3 = 0;
+        for (int g = 0; g < WARPS; ++g) {
+          f0 += sred[4 * g]; f1 += sred[4 * g + 1]; f2 += sred[4 * g + 2]; f3 += sred[4 * g + 3];
+        }
+        double* o = partials + ((size_t)kth * G + blockIdx.x) * 4;
+        o[0] = f0; o[1] = f1; o[2] = f2; o[3] = f3;
+      }
     }
   }
   if (red_out) finish_all(partials, int(G), K, NQ, with_cost, red_out, counter, p2p);

@@ -43,30 +43,29 @@ def test_state_matches_oracle_ansatz(dv):
 @pytest.mark.parametrize("n,layers,ent", [(7, 1, 0), (7, 5, 1), (8, 3, 0), (8, 4, 1), (9, 2, 1), (9, 9, 0),
                                           (10, 1, 0), (10, 10, 0), (10, 10, 1), (10, 40, 0)])
 def test_cluster_prefix_matches_oracle_and_single_cta(dv, n, layers, ent):
-    """a2 on a thread-block cluster of 2^(n-7) CTAs (DSMEM exchanges) vs the oracle's gate-by-gate
-    V(theta)|0> and vs the one-CTA prefix (the default; the cluster one is opts.prefix = 1), for both
-    entangling rings; a K = 3
-    batch checks that each theta's cluster writes its own state (terms of every theta)."""
+    """a2: the default one-CTA prefix (two amplitudes per thread), the thread-block cluster of
+    2^(n-7) CTAs (DSMEM exchanges, opts.prefix = 1) and the four-amplitude one-CTA kernel
+    (opts.prefix = 2) vs the oracle's gate-by-gate V(theta)|0>, for both entangling rings; a K = 3
+    batch checks that each theta's CTA / cluster writes its own state (costs of every theta)."""
     dvqls, _ = dv
     w = configs.random_workload(n, 2, layers, seed=40 + n, entangler=ent)
-    a = dvqls.from_workload(w, max_batch=3, prefix=1)
-    b = dvqls.from_workload(w, max_batch=3)
+    ctxs = [dvqls.from_workload(w, max_batch=3, prefix=p) for p in (0, 1, 2)]
     try:
         for s in (0, 1):
             th = w.theta0(s)
-            xa, xb = a.state(th), b.state(th)
             xr = sim.ansatz_state(n, layers, th, ent)
-            assert np.max(np.abs(xa - xr)) < 1e-12
-            assert np.max(np.abs(xb - xr)) < 1e-12
+            for c in ctxs:
+                assert np.max(np.abs(c.state(th) - xr)) < 1e-12
         ths = np.stack([w.theta0(s) for s in (2, 3, 4)])
-        ca, cb = a.cost_batch(ths)[0], b.cost_batch(ths)[0]
-        assert np.max(np.abs(ca - cb)) < 1e-12
+        cs = [c.cost_batch(ths)[0] for c in ctxs]
+        for c in cs[1:]:
+            assert np.max(np.abs(c - cs[0])) < 1e-12
         from oracle import cost as ocost
         for k in range(3):
-            assert abs(ca[k] - ocost.cost(sim.workload_terms(w, ths[k]), ocost.coeffs_of(w), n, w.L)[0]) < 1e-10
+            assert abs(cs[0][k] - ocost.cost(sim.workload_terms(w, ths[k]), ocost.coeffs_of(w), n, w.L)[0]) < 1e-10
     finally:
-        a.destroy()
-        b.destroy()
+        for c in ctxs:
+            c.destroy()
 
 
 def _solve_and_check(dvqls, optimize, w, gradient="fd"):
