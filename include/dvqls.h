@@ -130,11 +130,9 @@ typedef struct dvqls_opts {
                                   circuit per warp (plane_kernel), 2 = two circuits in flight per
                                   warp, skewed phases (plane2_kernel; measured 0.6-1.5 % faster).
                                   Bitwise-identical terms; (E, Psi) equal to rounding.          */
-  int prefix;                  /* V(theta)|0> for 7 <= n <= 10: 0 = one CTA per theta, two
-                                  amplitudes per thread (default); 1 = a thread-block cluster of
-                                  2^(n-7) CTAs per theta joined by DSMEM (measured no faster on
-                                  B200: DESIGN.md §6); 2 = one CTA, four amplitudes per thread
-                                  (the round-1 kernel)                                          */
+  int prefix;                  /* V(theta)|0> for 7 <= n <= 10: 0 = one CTA per theta (default);
+                                  1 = a thread-block cluster of 2^(n-7) CTAs per theta joined by
+                                  DSMEM (measured no faster on B200: DESIGN.md §6)              */
 } dvqls_opts;
 
 #define DVQLS_ALLREDUCE_P2P 0

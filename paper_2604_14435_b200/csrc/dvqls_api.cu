@@ -568,8 +568,8 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
     fail(ctx, DVQLS_E_ARG, "entangler must be 0 (CNOT ring) or 1 (CZ ring)");
     return bail(DVQLS_E_ARG);
   }
-  if (o.prefix < 0 || o.prefix > 2) {
-    fail(ctx, DVQLS_E_ARG, "prefix must be 0, 1 or 2");
+  if (o.prefix < 0 || o.prefix > 1) {
+    fail(ctx, DVQLS_E_ARG, "prefix must be 0 or 1");
     return bail(DVQLS_E_ARG);
   }
   if (o.variant < 0 || o.variant > 2) {
@@ -796,7 +796,7 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
 
   // ---- prefix (a2) ----------------------------------------------------------------------
   if (n <= 12) {
-    ctx->pc = prefix_cfg(n, layers, o.prefix);
+    ctx->pc = prefix_cfg(n, layers, o.prefix == 1);
     if (!ctx->pc.fn || cudaFuncSetAttribute(ctx->pc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             int(ctx->pc.smem)) != cudaSuccess) {
       fail(ctx, DVQLS_E_CUDA, "prefix kernel smem %zu B", ctx->pc.smem);

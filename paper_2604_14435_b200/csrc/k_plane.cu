@@ -45,11 +45,7 @@ KernelCfg plane2_cfg() {
   return k;
 }
 
-PrefixCfg prefix_cfg(int n, int layers, int variant) {
-  const bool cluster = variant == 1;
-  static const void* duos[11] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                 (const void*)&prefix_duo_kernel<7>, (const void*)&prefix_duo_kernel<8>,
-                                 (const void*)&prefix_duo_kernel<9>, (const void*)&prefix_duo_kernel<10>};
+PrefixCfg prefix_cfg(int n, int layers, bool cluster) {
   static const void* quads[11] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                                   (const void*)&prefix_quad_kernel<7>, (const void*)&prefix_quad_kernel<8>,
                                   (const void*)&prefix_quad_kernel<9>, (const void*)&prefix_quad_kernel<10>};
@@ -81,11 +77,7 @@ PrefixCfg prefix_cfg(int n, int layers, int variant) {
       return p;
     }
   }
-  if (n >= 7 && n <= 10 && variant != 2) {  // 2 amplitudes per thread (default)
-    p.fn = duos[n];
-    p.threads = int(N / 2);
-    p.smem = sizeof(double2) * (2 * N + 2 * size_t(n) * layers) + sizeof(int) * N;
-  } else if (n >= 7 && n <= 10) {  // 4 amplitudes per thread (opts.prefix = 2)
+  if (n >= 7 && n <= 10) {  // 4 amplitudes per thread, shuffles + 2 transposes per layer
     p.fn = quads[n];
     p.threads = std::max(32, int(N / 4));
     p.smem = sizeof(double2) * (2 * N + 2 * size_t(n) * layers) + sizeof(int) * N;

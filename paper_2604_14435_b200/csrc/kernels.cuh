@@ -288,11 +288,19 @@ prefix_lanes_kernel(int layers, int entangler, const double* __restrict__ thetas
 // and reused for the thread's 4 independent amplitudes (4x fewer SMEM wavefronts per
 // amplitude than one amplitude per thread; measured SMEM-bound otherwise).
 // ---------------------------------------------------------------------------
+// phase timestamps for tools/prefix_timing.cu (compiled with -DDVQLS_PREFIX_TS; no code otherwise)
+#ifdef DVQLS_PREFIX_TS
+__device__ long long g_prefix_ts[256];
+#define PREFIX_TS(k) do { if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_prefix_ts[(threadIdx.x >> 5) * 16 + (k)] = clock64(); } while (0)
+#else
+#define PREFIX_TS(k) do { } while (0)
+#endif
 __device__ __forceinline__ int qswz(int i) { return i ^ ((i >> 2) & 7) ^ ((i >> 7) & 7); }
 
 template <int NQ>
 __global__ void __launch_bounds__(256)
 prefix_quad_kernel(int layers, int entangler, const double* __restrict__ thetas, double2* __restrict__ x_all) {
+  PREFIX_TS(0);
   pdl_trigger();
   constexpr int n = NQ;
   constexpr int N = 1 << n;
@@ -383,12 +391,14 @@ prefix_quad_kernel(int layers, int entangler, const double* __restrict__ thetas,
     }
   };
 
+  PREFIX_TS(1);
   for (int layer = 0; layer < layers; ++layer) {
     const int gl = layer * n;  // gate of qubit q is gl + q, qubit q <-> position n - 1 - q
     reg_gate(gl + (n - 1 - 0), 0);
     reg_gate(gl + (n - 1 - 1), 1);
 #pragma unroll
     for (int pos = 2; pos < 7; ++pos) lane_gate(gl + (n - 1 - pos), pos - 2);
+    if (layer == 0) PREFIX_TS(2);
     // Buffer discipline: a buffer is rewritten only after a barrier that follows every read of
     // it (the reads of sbuf0 precede the barrier of sbuf1 and vice versa), so each transpose
     // needs a single barrier.  W = 0 (no warp bits): alternate the one transpose per layer.
@@ -415,150 +425,12 @@ prefix_quad_kernel(int layers, int entangler, const double* __restrict__ thetas,
       const double2 a = ring[pX[r]];
       v[r] = nX[r] ? make_double2(-a.x, -a.y) : a;
     }
+    if (layer == 0) PREFIX_TS(3);
   }
+  PREFIX_TS(4);
   double2* x = x_all + (size_t)blockIdx.x * N;
 #pragma unroll
   for (int r = 0; r < 4; ++r) x[iX0 | r] = v[r];
-}
-
-// ---------------------------------------------------------------------------
-// a2 for 7 <= n <= 10 (the default): TWO amplitudes per thread (2^(n-1) threads, 16 warps at
-// n = 10).  The same per-amplitude arithmetic as prefix_quad_kernel with twice the warps: the quad
-// kernel runs 2 warps per SM sub-partition and stalls on its own dependency chains (ncu: FP64 pipe
-// 42 %, short_scoreboard + wait 42 % of the stall samples, profiles/r2g/prefix_ncu_full.txt) --
-// the one-CTA prefix is latency-bound, not FP64-bound (its FP64 floor on one SM is ~6.5 us at cfg3).
-//   layout X: i = (w << 6) | (l << 1) | r     r: 1 register bit, l: 5 lane bits, w: W = n-6 bits
-//   layout Y: positions 6..n-1 on lane bits 0..W-1, positions 1..W on the warp bits
-// The 3G half-angle sines and cosines are computed one per thread (the quad kernel: three
-// sequential sincos per gate on G threads), staged in the still unused exchange buffers.
-// SMEM slot: the bits a quarter-warp varies in either layout (1..3 in X, 6..8 in Y) are folded
-// into bits 0..2, so the 16-byte accesses of both transposes are conflict-free.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int dswz(int i) { return i ^ ((i >> 3) & 1) ^ ((i >> 6) & 7); }
-
-template <int NQ>
-__global__ void __launch_bounds__(1 << (NQ - 1))
-prefix_duo_kernel(int layers, int entangler, const double* __restrict__ thetas, double2* __restrict__ x_all) {
-  pdl_trigger();
-  constexpr int n = NQ;
-  constexpr int N = 1 << n;
-  constexpr int W = n - 6;
-  constexpr int T = N / 2;
-  extern __shared__ double2 dsm[];
-  const int P = 3 * n * layers;
-  const int G = n * layers;
-  double2* sbuf0 = dsm;                      // 2 x N amplitudes: the two transposes of a layer
-  double2* sbuf1 = dsm + N;
-  double2* tabU = dsm + 2 * N;               // 2 per gate: a, b of U = [[a, -b*], [b, a*]]
-  int* perm = reinterpret_cast<int*>(tabU + 2 * G);
-  const double* th = thetas + (size_t)blockIdx.x * P;
-  const int tid = threadIdx.x;
-  const int l = tid & 31, w = tid >> 5;
-  const unsigned full = 0xffffffffu;
-
-  if (P <= 2 * N) {  // one sincos per thread into the exchange buffers, then the gate table
-    for (int j = tid; j < P; j += T) {
-      double sn, cs;
-      sincos(0.5 * th[j], &sn, &cs);
-      dsm[j] = make_double2(sn, cs);
-    }
-  }
-  for (int i = tid; i < N; i += T) {
-    int e = i;
-    if (entangler == 0) {
-      int j = i;  // new[i] = old[c_0(c_1(...c_{n-1}(i)))]
-#pragma unroll
-      for (int q = n - 1; q >= 0; --q) {
-        const int pc = n - 1 - q, pt = n - 1 - ((q + 1) % n);
-        if ((j >> pc) & 1) j ^= 1 << pt;
-      }
-      e = j;
-    } else {
-      int par = 0;
-#pragma unroll
-      for (int q = 0; q < n; ++q) par ^= ((i >> (n - 1 - q)) & (i >> (n - 1 - (q + 1) % n))) & 1;
-      e = int(unsigned(i) | (unsigned(par) << 31));
-    }
-    perm[i] = e;
-  }
-  __syncthreads();
-  for (int g = tid; g < G; g += T) {
-    double s0, c0, s1, c1, s2, c2;
-    if (P <= 2 * N) {
-      s0 = dsm[3 * g].x; c0 = dsm[3 * g].y;
-      s1 = dsm[3 * g + 1].x; c1 = dsm[3 * g + 1].y;
-      s2 = dsm[3 * g + 2].x; c2 = dsm[3 * g + 2].y;
-    } else {
-      sincos(0.5 * th[3 * g + 0], &s0, &c0);
-      sincos(0.5 * th[3 * g + 1], &s1, &c1);
-      sincos(0.5 * th[3 * g + 2], &s2, &c2);
-    }
-    tabU[2 * g + 0] = make_double2(c1 * (c2 * c0 - s2 * s0), -s1 * (c2 * c0 + s2 * s0));
-    tabU[2 * g + 1] = make_double2(c1 * (s2 * c0 + c2 * s0), s1 * (c2 * s0 - s2 * c0));
-  }
-  __syncthreads();  // gate table ready; the exchange buffers are free again
-
-  const int iX0 = (w << 6) | (l << 1);
-  const int iY0 = ((l >> W) << (1 + W)) | (w << 1) | ((l & ((1 << W) - 1)) << 6);
-  int pX[2];
-  bool nX[2];
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int e = perm[iX0 | r];
-    pX[r] = dswz(e & 0x7fffffff);
-    nX[r] = e < 0;
-  }
-  double2 v[2];
-#pragma unroll
-  for (int r = 0; r < 2; ++r) v[r] = make_double2((iX0 | r) == 0 ? 1.0 : 0.0, 0.0);
-
-  for (int layer = 0; layer < layers; ++layer) {
-    const int gl = layer * n;  // gate of qubit q is gl + q, qubit q <-> position n - 1 - q
-    {  // register bit (position 0): in-thread 2x2 complex matvec
-      const double2 ua = tabU[2 * (gl + n - 1)], ub = tabU[2 * (gl + n - 1) + 1];
-      const double2 x0 = v[0], x1 = v[1];
-      v[0] = make_double2(fma(ua.x, x0.x, fma(-ua.y, x0.y, fma(-ub.x, x1.x, -ub.y * x1.y))),
-                          fma(ua.x, x0.y, fma(ua.y, x0.x, fma(-ub.x, x1.y, ub.y * x1.x))));
-      v[1] = make_double2(fma(ub.x, x0.x, fma(-ub.y, x0.y, fma(ua.x, x1.x, ua.y * x1.y))),
-                          fma(ub.x, x0.y, fma(ub.y, x0.x, fma(ua.x, x1.y, -ua.y * x1.x))));
-    }
-    // lane bit LBIT: row of U selected by the thread's bit; partner amplitude by shuffle
-    auto lane_gate = [&](int g, int lbit) {
-      const double2 ua = tabU[2 * g], ub = tabU[2 * g + 1];
-      const bool bit = (l >> lbit) & 1;
-      const double2 cs = make_double2(ua.x, bit ? -ua.y : ua.y);
-      const double2 co = make_double2(bit ? ub.x : -ub.x, ub.y);
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const double2 pp =
-            make_double2(__shfl_xor_sync(full, v[r].x, 1 << lbit), __shfl_xor_sync(full, v[r].y, 1 << lbit));
-        const double sr = fma(cs.x, v[r].x, -cs.y * v[r].y), si = fma(cs.x, v[r].y, cs.y * v[r].x);
-        v[r] = make_double2(fma(co.x, pp.x, fma(-co.y, pp.y, sr)), fma(co.x, pp.y, fma(co.y, pp.x, si)));
-      }
-    };
-#pragma unroll
-    for (int pos = 1; pos < 6; ++pos) lane_gate(gl + (n - 1 - pos), pos - 1);
-    // X -> Y through sbuf0, gates on positions 6..n-1, Y -> sbuf1; the ring folded into the read
-    // back to X (buffer discipline as in prefix_quad_kernel: one barrier per transpose)
-#pragma unroll
-    for (int r = 0; r < 2; ++r) sbuf0[dswz(iX0 | r)] = v[r];
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < 2; ++r) v[r] = sbuf0[dswz(iY0 | r)];
-#pragma unroll
-    for (int pos = 6; pos < n; ++pos) lane_gate(gl + (n - 1 - pos), pos - 6);
-#pragma unroll
-    for (int r = 0; r < 2; ++r) sbuf1[dswz(iY0 | r)] = v[r];
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const double2 a = sbuf1[pX[r]];
-      v[r] = nX[r] ? make_double2(-a.x, -a.y) : a;
-    }
-  }
-  double2* x = x_all + (size_t)blockIdx.x * N;
-#pragma unroll
-  for (int r = 0; r < 2; ++r) x[iX0 | r] = v[r];
 }
 
 // ---------------------------------------------------------------------------

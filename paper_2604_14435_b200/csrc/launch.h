@@ -27,7 +27,7 @@ struct PrefixCfg {
   int cluster = 0;  // > 0: thread-block-cluster prefix (prefix_cluster.cuh), grid (cluster, K) with
                     // cluster dims (cluster, 1, 1), args (layers, entangler, thetas, x)
 };
-PrefixCfg prefix_cfg(int n, int layers, int variant);  // opts.prefix: 0 default, 1 cluster, 2 quad
+PrefixCfg prefix_cfg(int n, int layers, bool cluster = true);
 void launch_finalize(const double* ep, int K, int n, double* out, cudaStream_t st);
 
 // ---- k_onchip.cu: n = 11, 12 uniform b (onchip_plane.cuh) + its planar copy of x

@@ -135,7 +135,6 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
               const double2* __restrict__ hv, double hv_scale, int L, int64_t c0, int64_t C, int K,
               double* __restrict__ out_terms, double* __restrict__ partials, int with_cost,
               double* __restrict__ red_out, unsigned* __restrict__ counter, P2PArgs p2p) {
-  pdl_wait();
   (void)hv; (void)hv_scale;
   constexpr size_t SMALL = small_bytes<WARPS>();
   double* shalf = reinterpret_cast<double*>(dvqls_smem);  // [NP][2 parities][2 circuits]
@@ -178,6 +177,10 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
     if (k < th_first || k > th_last)
       for (int q = 0; q < 4; ++q) partials[(size_t(k) * G + blockIdx.x) * 4 + q] = 0.0;
   const int64_t tk0 = c0 >> 1;  // global task index of local task 0
+  // everything above overlaps the prefix kernel under programmatic dependent launch (it reads only
+  // launch arguments and writes partials, which the previous call finished with before the prefix
+  // started); x is read only after the prefix's completion
+  pdl_wait();
 
   for (int kth = th_first; kth <= th_last; ++kth) {
     const int64_t pa = max(Fb, int64_t(kth) * C) - int64_t(kth) * C;

@@ -43,13 +43,12 @@ def test_state_matches_oracle_ansatz(dv):
 @pytest.mark.parametrize("n,layers,ent", [(7, 1, 0), (7, 5, 1), (8, 3, 0), (8, 4, 1), (9, 2, 1), (9, 9, 0),
                                           (10, 1, 0), (10, 10, 0), (10, 10, 1), (10, 40, 0)])
 def test_cluster_prefix_matches_oracle_and_single_cta(dv, n, layers, ent):
-    """a2: the default one-CTA prefix (two amplitudes per thread), the thread-block cluster of
-    2^(n-7) CTAs (DSMEM exchanges, opts.prefix = 1) and the four-amplitude one-CTA kernel
-    (opts.prefix = 2) vs the oracle's gate-by-gate V(theta)|0>, for both entangling rings; a K = 3
+    """a2: the default one-CTA prefix and the thread-block cluster of 2^(n-7) CTAs (DSMEM exchanges,
+    opts.prefix = 1) vs the oracle's gate-by-gate V(theta)|0>, for both entangling rings; a K = 3
     batch checks that each theta's CTA / cluster writes its own state (costs of every theta)."""
     dvqls, _ = dv
     w = configs.random_workload(n, 2, layers, seed=40 + n, entangler=ent)
-    ctxs = [dvqls.from_workload(w, max_batch=3, prefix=p) for p in (0, 1, 2)]
+    ctxs = [dvqls.from_workload(w, max_batch=3, prefix=p) for p in (0, 1)]
     try:
         for s in (0, 1):
             th = w.theta0(s)

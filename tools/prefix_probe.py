@@ -1,6 +1,5 @@
-"""Prefix kernels of cfg3 (n = 10, d = 10) for profiling / timing: the one-CTA prefix with two
-amplitudes per thread (default), the cluster prefix (opts.prefix = 1) and the one-CTA four-amplitude
-kernel (opts.prefix = 2), K thetas per call, timing events on (per-kernel times).
+"""Prefix kernels of cfg3 (n = 10, d = 10) for profiling / timing: the one-CTA prefix (default) and
+the cluster prefix (opts.prefix = 1), K thetas per call, timing events on (per-kernel times).
 
     python tools/prefix_probe.py [K]
 """
@@ -23,7 +22,7 @@ w = configs.cfg3()
 th = torch.tensor(np.stack([w.theta0(s) for s in range(K)]), dtype=torch.float64, device="cuda")
 out = torch.empty(5 * K, dtype=torch.float64, device="cuda")
 res = {}
-for name, pf in (("cluster", 1), ("quad", 2), ("duo", 0)):
+for name, pf in (("cluster", 1), ("one_cta", 0)):
     ctx = dvqls.from_workload(w, max_batch=K, timing=True, prefix=pf)
     ms = []
     for i in range(30):
