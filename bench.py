@@ -25,6 +25,7 @@ The oracle (oracle/, test infrastructure) is only executed for `cpu_baseline`
 from __future__ import annotations
 
 import argparse
+import csv
 import json
 import os
 import statistics
@@ -201,8 +202,7 @@ def streaming_roofline(w, local_c, KT, had_ms, peaks, peak_src, grid=None):
            "note": (f"algorithmic DRAM bytes per launch = {b:.4g} (64N per numerator circuit: 3 passes "
                     f"through the per-CTA scratch, x L2-resident; n >= 23: 160N + 32N per denominator) / mean "
                     f"CUDA-event kernel time; peak = hbm_gbs of {peak_src} MEASURED_PEAKS.json. model96_GBps "
-                    f"= the SURVEY §8(d) 96N model (x reads counted as HBM); traffic: ncu dram bytes are "
-                    f"in profiles/ (not measured inside this run)")}
+                    f"= the SURVEY §8(d) 96N model (x reads counted as HBM); traffic: traffic_note")}
     if grid is not None:
         scratch = grid * (1 << w.n) * 8
         out["scratch_bytes"] = scratch
@@ -235,11 +235,51 @@ def onchip_roofline(w, local_c, KT, had_ms, sms, fmax, peak_src, kernel):
             "note": (f"{main['note']} / mean CUDA-event time of the kernel on the launching stream (probe "
                      f"context, same run); peak = {'128 B' if smem_binds else '64 lanes'}/clk/SM x {sms} SMs x "
                      f"sm_max_mhz ({peak_src} MEASURED_PEAKS.json; per-SM rates confirmed by "
-                     f"tools/microbench.cu, profiles/r1_microbench.json). traffic: ncu dram bytes are in "
-                     f"profiles/ (the kernel reads x, 16 KB per theta, and writes its terms)")}
+                     f"tools/microbench.cu, profiles/r1_microbench.json). traffic: traffic_note (the kernel "
+                     f"reads x, 16 KB per theta, and writes its terms)")}
 
 
 # ----------------------------------------------------------------------------------------------
+def measure_traffic(args, kernel):
+    """roofline.traffic of THIS run's code and configuration: DRAM bytes (read + write) of the
+    dominant kernel per launch, from ncu (dram__bytes_read.sum + dram__bytes_write.sum) on a child
+    `bench.py --traffic-probe` with the same configuration (two calls of the measured launch
+    sequence; the second launch is captured).  Never timed: the throughput numbers come from the
+    uninstrumented run.  Returns (bytes or None, note)."""
+    import shutil
+    import subprocess
+    import tempfile
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    if ncu is None:
+        return None, "ncu not found on this box"
+    name = kernel.split("<")[0]
+    fwd = ["--config", args.config, "--batch", str(args.batch), "--n", str(args.n), "--variant", str(args.variant),
+           "--allreduce", args.allreduce] + (["--no-graphs"] if args.no_graphs else [])
+    with tempfile.TemporaryDirectory() as td:
+        log = os.path.join(td, "ncu.csv")
+        cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--print-units", "base", "--csv",
+               "-k", f"regex:{name}", "-s", "1", "-c", "1", "--log-file", log,
+               sys.executable, os.path.abspath(__file__), *fwd, "--traffic-probe"]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+            rows = list(csv.reader(open(log))) if os.path.exists(log) else []
+        except (OSError, subprocess.SubprocessError) as e:
+            return None, f"ncu capture failed: {type(e).__name__}"
+    vals = {}
+    for row in rows:
+        if len(row) >= 15 and row[12] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            try:
+                vals[row[12]] = float(row[14].replace(",", ""))
+            except ValueError:
+                pass
+    if len(vals) != 2:
+        return None, f"ncu capture failed (rc {r.returncode}): {(r.stderr or r.stdout)[-200:].strip()}"
+    return (vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
+            f"DRAM bytes (read {vals['dram__bytes_read.sum']:.4g} + write {vals['dram__bytes_write.sum']:.4g}) "
+            f"of one {name} launch of this configuration, ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
+            "on a --traffic-probe child of this run (not timed)")
+
+
 def _sized_sample(w, theta, mode, cores, target_s):
     """Evenly strided circuit sample whose oracle run takes ~target_s on `cores` threads: the sample
     doubles until one run takes >= 1 s, then it is scaled to the target (capped at the workload)."""
@@ -338,6 +378,8 @@ def main():
     ap.add_argument("--variant", type=int, default=0, help="n = 10 kernel variant (dvqls_opts.variant)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-next2", action="store_true", help="skip the NEXT-2 fast-path side measurement")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic capture of the kernel")
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)  # run under ncu by measure_traffic
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = CONFIGS[args.config](args.n) if args.config.startswith("cfg5") else CONFIGS[args.config]()
@@ -388,6 +430,15 @@ def main():
                              max_batch=max(KT, 1), workspace=workspace, **vopts)
 
     ctx = make_ctx(False, nccl_ids[0])   # the measured path: CUDA graph per call, PDL between prefix and kernel
+    if args.traffic_probe:  # two calls of the measured launch sequence for ncu (measure_traffic), nothing else
+        th = torch.tensor(np.stack([w.theta0(s) for s in range(KT)]), dtype=torch.float64, device=dev)
+        out = torch.empty(5 * KT, dtype=torch.float64, device=dev)
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                ctx.cost_dev(KT, th, out)
+        torch.cuda.synchronize()
+        ctx.destroy()
+        return 0
     pctx = make_ctx(True, nccl_ids[1])   # probe: CUDA events between the kernels (per-kernel times, roofline)
     c0, c1 = ctx.local_range()
     thetas = np.stack([w.theta0(s) for s in range(KT)])
@@ -671,6 +722,8 @@ def main():
             "next3_global": next3,
             "next4_decompose": next4,
         }
+        if world == 1 and not args.no_traffic:
+            roof["traffic"], roof["traffic_note"] = measure_traffic(args, roof["kernel"])
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(w, thetas[0])
         print(json.dumps(line), flush=True)

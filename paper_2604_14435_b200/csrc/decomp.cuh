@@ -243,7 +243,12 @@ sort_emit_kernel(const double2* __restrict__ C, int n, const uint64_t* __restric
   {  // ||c||_2 = sqrt(sum_m sq[m]) in a fixed order (strided partials, then a tree); SMEM reused below
     double* red = reinterpret_cast<double*>(sort_smem);
     double a = 0.0;
-    for (uint32_t i = threadIdx.x; i < (1u << n); i += THREADS) a += sq[i];
+    const uint32_t nm = 1u << n, per = (nm + THREADS - 1) / THREADS;  // a contiguous chunk per thread,
+#pragma unroll 8
+    for (uint32_t j = 0; j < per; ++j) {                               // its loads issued together
+      const uint32_t i = threadIdx.x * per + j;
+      if (i < nm) a += sq[i];
+    }
     red[threadIdx.x] = a;
     __syncthreads();
     for (int off = THREADS / 2; off >= 1; off >>= 1) {
@@ -316,7 +321,12 @@ sort_emit_kernel(const double2* __restrict__ C, int n, const uint64_t* __restric
 __global__ void __launch_bounds__(THREADS) norm_kernel(const double* __restrict__ sq, int n, double* __restrict__ norm) {
   __shared__ double red[THREADS];
   double a = 0.0;
-  for (uint32_t i = threadIdx.x; i < (1u << n); i += THREADS) a += sq[i];
+  const uint32_t nm = 1u << n, per = (nm + THREADS - 1) / THREADS;
+#pragma unroll 8
+  for (uint32_t j = 0; j < per; ++j) {
+    const uint32_t i = threadIdx.x * per + j;
+    if (i < nm) a += sq[i];
+  }
   red[threadIdx.x] = a;
   __syncthreads();
   for (int off = THREADS / 2; off >= 1; off >>= 1) {
