@@ -8,7 +8,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TA
 timeout 2400 python -m pytest tests -m gpu -q -rs --durations=25 > gpurun_out/${TAG}_pytest.log 2>&1
 timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err
-B="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-next2"
+B="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-next2 --no-traffic"
 timeout 300 $B > gpurun_out/${TAG}_b5.json 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"plane2_kernel" -c 1 -o gpurun_out/${TAG}_prof $B > gpurun_out/${TAG}_ncu.log 2>&1
