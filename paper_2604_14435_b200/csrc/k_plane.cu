@@ -106,6 +106,14 @@ static __global__ void finalize_kernel(const double* __restrict__ ep, int K, int
 }
 
 
+#ifdef DVQLS_PLANE2_TS
+void* plane2_ts_ptr() {
+  void* p = nullptr;
+  cudaGetSymbolAddress(&p, plane2::g_p2ts);
+  return p;
+}
+#endif
+
 void launch_finalize(const double* ep, int K, int n, double* out, cudaStream_t st) {
   finalize_kernel<<<(K + 255) / 256, 256, 0, st>>>(ep, K, n, out);
 }

@@ -43,6 +43,21 @@ using plane::XREG;
 constexpr int WARPS = 12;
 constexpr int NP = WARPS / 2;
 
+// %globaltimer stamps per CTA for tools/plane2_timing.cu (built with -DDVQLS_PLANE2_TS only):
+// [0] entry, [1] after pdl_wait, [2] x staged, [3] all tasks of the last piece done, [4] piece
+// reduction written, [5] kernel end of the CTA, [6 + pair] the pair's last task done
+#ifdef DVQLS_PLANE2_TS
+__device__ unsigned long long g_p2ts[160 * 16];
+__device__ __forceinline__ void p2ts(int k) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_p2ts[blockIdx.x * 16 + k] = t;
+}
+#define P2TS(k) p2ts(k)
+#else
+#define P2TS(k) do { } while (0)
+#endif
+
 template <int B0, int B1>
 __device__ __forceinline__ void fwht(double (&v)[R]) { plane::fwht<B0, B1>(v); }
 
@@ -136,6 +151,7 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
               double* __restrict__ out_terms, double* __restrict__ partials, int with_cost,
               double* __restrict__ red_out, unsigned* __restrict__ counter, P2PArgs p2p) {
   (void)hv; (void)hv_scale;
+  if (threadIdx.x == 0) P2TS(0);
   constexpr size_t SMALL = small_bytes<WARPS>();
   double* shalf = reinterpret_cast<double*>(dvqls_smem);  // [NP][2 parities][2 circuits]
   double* sred = shalf + NP * 4;                            // [WARPS][4]
@@ -181,6 +197,7 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
   // launch arguments and writes partials, which the previous call finished with before the prefix
   // started); x is read only after the prefix's completion
   pdl_wait();
+  if (threadIdx.x == 0) P2TS(1);
 
   for (int kth = th_first; kth <= th_last; ++kth) {
     const int64_t pa = max(Fb, int64_t(kth) * C) - int64_t(kth) * C;
@@ -198,6 +215,7 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
     }
     if (threadIdx.x == 0) *sctr = ta;
     __syncthreads();
+    if (threadIdx.x == 0) P2TS(2);
 
     // one task (Re and Im circuit) per iteration; one copy of each path (instruction-cache footprint)
     int prev = -1;
@@ -213,7 +231,10 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
         terms[2 * prev + int(t)] = (t == 0 ? pha : phb) + sh[t];
       }
       const int task = stask[2 * pair + par];
-      if (task >= tb) break;
+      if (task >= tb) {
+        if (pl == 0 && t == 0) P2TS(6 + pair);
+        break;
+      }
       const int64_t tk = tk0 + task, lk = tk / n1;
       const int s_ = int(tk - lk * n1);
       const int kq = int(lk % L), lq = int(lk / L);
@@ -286,6 +307,7 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
       prev = task;
     }
     __syncthreads();  // every term of the piece is in out_terms
+    if (threadIdx.x == 0) P2TS(3);
     // a9: sum_c c_l^* c_k term_c over the piece [pa, pb) in a fixed order
     {
       double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
@@ -316,10 +338,12 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
         }
         double* o = partials + ((size_t)kth * G + blockIdx.x) * 4;
         o[0] = f0; o[1] = f1; o[2] = f2; o[3] = f3;
+        P2TS(4);
       }
     }
   }
   if (red_out) finish_all(partials, int(G), K, NQ, with_cost, red_out, counter, p2p);
+  if (threadIdx.x == 0) P2TS(5);
 }
 
 // dynamic SMEM to request when the dynamic base sits at shared-window address sb
