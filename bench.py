@@ -254,7 +254,7 @@ def measure_traffic(args, kernel):
         return None, "ncu not found on this box"
     name = kernel.split("<")[0]
     fwd = ["--config", args.config, "--batch", str(args.batch), "--n", str(args.n), "--variant", str(args.variant),
-           "--allreduce", args.allreduce] + (["--no-graphs"] if args.no_graphs else [])
+           "--allreduce", args.allreduce, "--stream-grid", str(args.stream_grid)] + (["--no-graphs"] if args.no_graphs else [])
     with tempfile.TemporaryDirectory() as td:
         log = os.path.join(td, "ncu.csv")
         cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--print-units", "base", "--csv",
@@ -376,6 +376,7 @@ def main():
                     help="cross-rank reduction: fused into the kernel tail over NVLink peer memory, or NCCL")
     ap.add_argument("--no-graphs", action="store_true", help="plain launches instead of one CUDA graph per call")
     ap.add_argument("--variant", type=int, default=0, help="n = 10 kernel variant (dvqls_opts.variant)")
+    ap.add_argument("--stream-grid", type=int, default=0, help="cap on the streaming kernels' CTAs (dvqls_opts.stream_grid)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-next2", action="store_true", help="skip the NEXT-2 fast-path side measurement")
     ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic capture of the kernel")
@@ -414,7 +415,7 @@ def main():
     KT = args.batch
     chars, co = w.arrays()
     vopts = {"allreduce": dvqls.DVQLS_ALLREDUCE_NCCL if args.allreduce == "nccl" else dvqls.DVQLS_ALLREDUCE_P2P,
-             "graphs": not args.no_graphs, "variant": args.variant}
+             "graphs": not args.no_graphs, "variant": args.variant, "stream_grid": args.stream_grid}
     if args.slice > 1:  # 1-GPU weak-scaling reference: rank 0's block of a SLICE-way split (virtual rank)
         if world > 1:
             raise SystemExit("--slice is the 1-GPU weak-scaling reference")
