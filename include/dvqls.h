@@ -186,7 +186,11 @@ int dvqls_cost(dvqls_ctx* ctx, const double* theta, double* out_cost, double* ou
 /* K independent thetas in one pass (FD / parameter-shift points), host buffers.
  *   thetas     K*P doubles, row-major;  1 <= K <= opts.max_batch
  *   out_costs  K doubles;  out_E_Psi NULL or 4*K doubles
- * Degenerate entries get NaN and the call returns DVQLS_E_DEGENERATE. */
+ * Degenerate entries get NaN and the call returns DVQLS_E_DEGENERATE.
+ * One CUDA graph launch per call: the inputs are copied into the context's mapped pinned stage;
+ * on a single rank the kernels read theta from it and write the results into it (no copy
+ * nodes), across ranks theta goes H2D and the results (with the error word) D2H inside the
+ * graph.  dvqls_cost is this call with K = 1. */
 int dvqls_cost_batch(dvqls_ctx* ctx, int K, const double* thetas, double* out_costs,
                      double* out_E_Psi);
 

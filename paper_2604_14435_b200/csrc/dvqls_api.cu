@@ -90,7 +90,8 @@ struct dvqls_ctx {
   unsigned* d_err = nullptr;     // (unsigned*)d_outbuf: sticky fused-allreduce timeout flag
   unsigned long long* d_epochs = nullptr;  // max_batch fused-allreduce epochs
   double* d_gather = nullptr;    // world * chunk (NCCL terms allgather)
-  double* h_stage = nullptr;     // pinned staging
+  double* h_stage = nullptr;     // pinned staging (mapped: h_stage_dev is its device alias)
+  double* h_stage_dev = nullptr;
   size_t h_stage_bytes = 0;
   unsigned* d_counter = nullptr; // last-CTA tickets, one per theta slot
   // fused NVLink allreduce (world > 1): own symmetric buffer + IPC-mapped peer buffers
@@ -887,8 +888,9 @@ int create_impl(dvqls_ctx** out, int n, int layers, int L, const char* paulis, c
   ctx->d_out = ctx->d_outbuf + 1;
   ctx->d_err = reinterpret_cast<unsigned*>(ctx->d_outbuf);
   ctx->h_stage_bytes = sizeof(double) * std::max<size_t>({size_t(KB) * (ctx->P + 5) + 1, 2 * size_t(ctx->P) + 6, 64});
-  if (cudaMallocHost((void**)&ctx->h_stage, ctx->h_stage_bytes) != cudaSuccess) {
-    fail(ctx, DVQLS_E_CUDA, "cudaMallocHost failed");
+  if (cudaHostAlloc((void**)&ctx->h_stage, ctx->h_stage_bytes, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&ctx->h_stage_dev, ctx->h_stage, 0) != cudaSuccess) {
+    fail(ctx, DVQLS_E_CUDA, "cudaHostAlloc (mapped) failed");
     return bail(DVQLS_E_CUDA);
   }
   // tables and counters are written on the context stream (the stream every later call uses)
@@ -1112,8 +1114,18 @@ int dvqls_cost_batch(dvqls_ctx* ctx, int K, const double* thetas, double* out_co
   if (int rc = check_usable(ctx)) return rc;
   const size_t tb = sizeof(double) * size_t(K) * ctx->P;
   std::memcpy(ctx->h_stage, thetas, tb);
-  // theta H2D from the pinned stage, the whole path, results D2H: one graph launch per call
   double* h = ctx->h_stage + size_t(K) * ctx->P;
+  if (ctx->world == 1 && ctx->vworld <= 1) {
+    // zero copy: the prefix reads theta from the mapped pinned stage and the fused reduction writes
+    // (C, E, Psi) straight into it -- one graph of two kernels, no copy nodes on the call path (the
+    // error word is only ever set by the cross-rank reduction, so a single rank leaves it 0)
+    std::memset(h, 0, sizeof(double));
+    double* hd = ctx->h_stage_dev + size_t(K) * ctx->P;
+    int rc = run_graph(ctx, 4, K, ctx->h_stage, h, [&] { return launch_eval(ctx, K, ctx->h_stage_dev, true, hd + 1); });
+    if (rc) return rc;
+    return finish_host_cost(ctx, K, out_costs, out_E_Psi);
+  }
+  // theta H2D from the pinned stage, the whole path, results D2H: one graph launch per call
   int rc = run_graph(ctx, 3, K, ctx->h_stage, h, [&] {
     CK(cudaMemcpyAsync(ctx->d_theta, ctx->h_stage, tb, cudaMemcpyHostToDevice, ctx->stream));
     int r = launch_eval(ctx, K, ctx->d_theta, true, ctx->d_out);
