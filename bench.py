@@ -240,6 +240,24 @@ def onchip_roofline(w, local_c, KT, had_ms, sms, fmax, peak_src, kernel):
 
 
 # ----------------------------------------------------------------------------------------------
+def parse_ncu_dram(rows):
+    """{metric: value} of dram__bytes_read.sum / dram__bytes_write.sum from the rows of an
+    `ncu --csv --print-units base` log (columns ... "Metric Name", "Metric Unit", "Metric Value";
+    the ==PROF== lines and other metrics are skipped; the first captured launch wins)."""
+    vals, hdr = {}, None
+    for row in rows:
+        if hdr is None:
+            if "Metric Name" in row and "Metric Value" in row:
+                hdr = (row.index("Metric Name"), row.index("Metric Value"))
+            continue
+        if len(row) > max(hdr) and row[hdr[0]] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            try:
+                vals.setdefault(row[hdr[0]], float(row[hdr[1]].replace(",", "")))
+            except ValueError:
+                pass
+    return vals
+
+
 def measure_traffic(args, kernel):
     """roofline.traffic of THIS run's code and configuration: DRAM bytes (read + write) of the
     dominant kernel per launch, from ncu (dram__bytes_read.sum + dram__bytes_write.sum) on a child
@@ -265,13 +283,7 @@ def measure_traffic(args, kernel):
             rows = list(csv.reader(open(log))) if os.path.exists(log) else []
         except (OSError, subprocess.SubprocessError) as e:
             return None, f"ncu capture failed: {type(e).__name__}"
-    vals = {}
-    for row in rows:
-        if len(row) >= 15 and row[12] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            try:
-                vals[row[12]] = float(row[14].replace(",", ""))
-            except ValueError:
-                pass
+    vals = parse_ncu_dram(rows)
     if len(vals) != 2:
         return None, f"ncu capture failed (rc {r.returncode}): {(r.stderr or r.stdout)[-200:].strip()}"
     return (vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],

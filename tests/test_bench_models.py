@@ -56,3 +56,26 @@ def test_onchip_roofline_reports_the_binding_model():
     assert r["bound"] == "smem" and r["unit"] == "GB/s"
     assert abs(r["frac"] - r["model_frac"]) < 1e-12
     assert r["fp64"]["frac"] < r["frac"] and r["traffic"] is None
+
+
+def test_parse_ncu_dram_csv():
+    """roofline.traffic comes from an ncu CSV log of a --traffic-probe child (bench.measure_traffic):
+    the parser finds the two DRAM metrics by the header's column names, skips ==PROF== lines and
+    other metrics, keeps the first launch's values and survives thousands separators."""
+    import csv
+    import io
+    log = (
+        '==PROF== Connected to process 1\n'
+        '"ID","Process ID","Process Name","Host Name","Kernel Name","Context","Stream","Block Size",'
+        '"Grid Size","Device","CC","Section Name","Metric Name","Metric Unit","Metric Value"\n'
+        '"0","1","python3","h","plane2_kernel","1","13","(384, 1, 1)","(148, 1, 1)","0","10.0",'
+        '"Command line profiler metrics","dram__bytes_read.sum","byte","352,768"\n'
+        '"0","1","python3","h","plane2_kernel","1","13","(384, 1, 1)","(148, 1, 1)","0","10.0",'
+        '"Command line profiler metrics","dram__bytes_write.sum","byte","0"\n'
+        '"0","1","python3","h","plane2_kernel","1","13","(384, 1, 1)","(148, 1, 1)","0","10.0",'
+        '"Command line profiler metrics","gpu__time_duration.sum","nsecond","4300000"\n'
+        '"1","1","python3","h","plane2_kernel","1","13","(384, 1, 1)","(148, 1, 1)","0","10.0",'
+        '"Command line profiler metrics","dram__bytes_read.sum","byte","999"\n')
+    vals = bench.parse_ncu_dram(list(csv.reader(io.StringIO(log))))
+    assert vals == {"dram__bytes_read.sum": 352768.0, "dram__bytes_write.sum": 0.0}
+    assert bench.parse_ncu_dram([["==PROF== nothing"]]) == {}
