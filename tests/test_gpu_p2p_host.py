@@ -1,5 +1,5 @@
 """GPU: the fused NVLink/peer-memory reduction (a10; "Global Reduction", Alg. 1 Step 4c
-P:461-463) with TWO processes on ONE GPU, bootstrapped through the caller's host allgather
+P:461-463) with 2, 3 and 8 processes on ONE GPU, bootstrapped through the caller's host allgather
 (dvqls_opts.host_allgather over torch.distributed gloo) instead of NCCL, so the kernel-tail
 reduction runs on the driver's single-GPU box:
 
@@ -81,7 +81,7 @@ def _worker(rank, world, port, case, out):
         dist.destroy_process_group()
 
 
-def _run(case):
+def _run(case, world=2):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -89,25 +89,29 @@ def _run(case):
     build.build()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(2, _free_port(), case, out), nprocs=2, join=True)
-    return {r: out[r] for r in range(2)}
+    mp.spawn(_worker, args=(world, _free_port(), case, out), nprocs=world, join=True)
+    return {r: out[r] for r in range(world)}
 
 
-@pytest.mark.parametrize("case", ["n6", "cfg3", "n13"])
-def test_two_processes_one_gpu_fused_reduction(case):
+@pytest.mark.parametrize("case,world", [("n6", 2), ("cfg3", 2), ("n13", 2), ("n6", 3), ("n6", 8)])
+def test_processes_one_gpu_fused_reduction(case, world):
+    """world 2 (each case), 3 (uneven task blocks) and 8 (the box's full rank count: 7 peers mapped
+    per rank, 8 epoch slots per theta)"""
     from dvqls_inputs import configs
     from oracle import cost as ocost
     from oracle import sim
 
-    res = _run(case)
+    res = _run(case, world)
     w = {"n6": lambda: configs.random_workload(6, 3, 2, seed=5), "cfg3": configs.cfg3,
          "n13": lambda: configs.random_workload(13, 2, 1, seed=6)}[case]()
     th = w.theta0()
     ref = sim.workload_terms(w, th)
     co = ocost.coeffs_of(w)
     Cr, Er, Pr = ocost.cost(ref, co, w.n, w.L)
-    assert res[0]["range"][0] == 0 and res[0]["range"][1] == res[1]["range"][0]
-    for r in range(2):
+    assert res[0]["range"][0] == 0 and res[world - 1]["range"][1] == w.n_circuits
+    for r in range(world - 1):
+        assert res[r]["range"][1] == res[r + 1]["range"][0]
+    for r in range(world):
         assert np.max(np.abs(res[r]["terms"] - ref)) <= 1e-10
         assert abs(res[r]["C"] - Cr) <= 1e-10 and abs(res[r]["E"] - Er) <= 1e-10 * max(1, abs(Er))
         for k in range(3):
@@ -115,7 +119,8 @@ def test_two_processes_one_gpu_fused_reduction(case):
             assert abs(res[r]["batch"][k] - Ck) <= 1e-10
             assert res[r]["dev"][5 * k] == res[r]["batch"][k]
         assert res[r]["graphs"] >= 1
-    assert res[0]["C"] == res[1]["C"] and np.array_equal(res[0]["dev"], res[1]["dev"])
+    for r in range(1, world):
+        assert res[0]["C"] == res[r]["C"] and np.array_equal(res[0]["dev"], res[r]["dev"])
 
 
 def test_peer_timeout_is_an_error_not_nan():
