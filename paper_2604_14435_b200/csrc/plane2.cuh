@@ -17,7 +17,8 @@
 //     seg 5: F4(A)           | X2(B)
 //     seg 6: readout(A)      | F4(B)
 //     seg 7: readout(B)
-// (F = five register butterfly stages, X = exchange through the warp's padded buffer, Z = c-Z_j).
+// (F = five register butterfly stages, X = exchange through the warp's padded buffer, Z = c-Z_j,
+// applied inside F3's or F4's stage on bit j as the sign of that stage's butterflies: fwht_z).
 // Two 32-double planes per thread (168 registers): 12 warps (6 pairs, 12 circuits in flight per
 // SM), one exchange buffer per warp (the segments use it in turn, guarded by __syncwarp).
 #pragma once
@@ -61,6 +62,27 @@ __device__ __forceinline__ void p2ts(int k) {
 template <int B0, int B1>
 __device__ __forceinline__ void fwht(double (&v)[R]) { plane::fwht<B0, B1>(v); }
 
+// a6 folded into the FWHT: c-Z_j negates every amplitude whose index bit p is set, and the
+// butterflies on the other bits commute with that diagonal sign, so it is applied inside the
+// stage on bit p as (a, b) -> (a - b, a + b) -- fma(+-1, b, a), bitwise the result of negating b
+// first (no separate pass of 64 integer sign flips per plane).  ZB = that stage's register bit in
+// [B0, B1), or -1 (none here).
+template <int B0, int B1>
+__device__ __forceinline__ void fwht_z(double (&v)[R], int zb) {
+#pragma unroll
+  for (int bb = B0; bb < B1; ++bb) {
+    const double sg = bb == zb ? -1.0 : 1.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (!(r & (1 << bb))) {
+        const double a = v[r], b = v[r | (1 << bb)];
+        v[r] = fma(sg, b, a);
+        v[r | (1 << bb)] = fma(-sg, b, a);
+      }
+    }
+  }
+}
+
 // a4: phi_i = sgn_k(i ^ m_k) x_pl[i ^ m_k] in layout A (sign and plane are address bits)
 __device__ __forceinline__ void gather(double (&v)[R], uint32_t xa, uint32_t pl, uint32_t t, const PauliTerm& Tk) {
   const uint32_t mh = Tk.xm >> TB, tl = t ^ (Tk.xm & 31u), zh = Tk.zm >> TB;
@@ -92,17 +114,6 @@ __device__ __forceinline__ void load_A(double (&v)[R], uint32_t baseA) {
 __device__ __forceinline__ void load_B(double (&v)[R], uint32_t baseB) {
 #pragma unroll
   for (int r = 0; r < R; ++r) v[r] = lds_a(baseB + uint32_t(r) * 8u);
-}
-
-// a6: c-Z_j in layout B (i = t << 5 | r: register bit p, or lane bit p - 5), branch-free: bit r of w
-// says whether register r flips, so the code after it is not duplicated per p
-__device__ __forceinline__ void zflip(double (&v)[R], int p, uint32_t t) {
-  // column word of register bit p: 0xAAAAAAAA, 0xCCCCCCCC, 0xF0F0F0F0, 0xFF00FF00, 0xFFFF0000
-  const uint32_t cols = p == 0 ? 0xAAAAAAAAu : p == 1 ? 0xCCCCCCCCu : p == 2 ? 0xF0F0F0F0u : p == 3 ? 0xFF00FF00u
-                                                                                              : 0xFFFF0000u;
-  const uint32_t w = p < RB ? cols : (((t >> (p - RB)) & 1u) ? 0xFFFFFFFFu : 0u);
-#pragma unroll
-  for (int r = 0; r < R; ++r) v[r] = flip(v[r], (w << (31 - r)) & 0x80000000u);
 }
 
 // a8: this plane's half of Re(i^q S), S = sum_j conj(x'_j) phi_j (plane.cuh), warp-summed
@@ -255,33 +266,34 @@ plane2_kernel(const double2* __restrict__ x_all, const PauliTerm* __restrict__ t
         __syncwarp();
         load_B(va, baseB);
         fwht<3, RB>(vb);
+        // Z_j's stage: index bit p is register bit p of layout B (F3) for p < 5, register bit
+        // p - 5 of layout A (F4) otherwise
+        const int z3 = p < RB ? p : -1, z4 = p < RB ? -1 : p - RB;
         // seg 3: F2 Z F3 (A) | X1(B)
         __syncwarp();
         store_A(vb, baseA);
         fwht<0, TB>(va);
-        zflip(va, p, t);
         __syncwarp();
         load_B(vb, baseB);
-        fwht<0, TB>(va);
+        fwht_z<0, TB>(va, z3);
         // seg 4: X2(A) | F2 Z F3 (B)
         __syncwarp();
         store_B(va, baseB);
         fwht<0, TB>(vb);
-        zflip(vb, p, t);
         __syncwarp();
         load_A(va, baseA);
-        fwht<0, TB>(vb);
+        fwht_z<0, TB>(vb, z3);
         // seg 5: F4(A) | X2(B)
         __syncwarp();
         store_B(vb, baseB);
-        fwht<0, 3>(va);
+        fwht_z<0, 3>(va, z4);
         __syncwarp();
         load_A(vb, baseA);
-        fwht<3, RB>(va);
+        fwht_z<3, RB>(va, z4);
         // seg 6: readout(A) | F4(B);  seg 7: readout(B)
         const int qa = (Tk.ny + Tl.ny) & 3, qb = (Tk.ny + Tl.ny + 3) & 3;
         ha = readout(va, xa, pl, t, Tl, qa);
-        fwht<0, RB>(vb);
+        fwht_z<0, RB>(vb, z4);
         hb = readout(vb, xa, pl, t, Tl, qb);
         constexpr double sc = 1.0 / double(N);
         ha *= (qa == 1 || qa == 2) ? -sc : sc;
