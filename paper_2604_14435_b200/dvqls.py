@@ -128,8 +128,10 @@ def load():
     L.dvqls_destroy.argtypes = [vp]
     L.dvqls_destroy.restype = None
     L.dvqls_terms.argtypes = [vp, dp, dp]
-    L.dvqls_cost.argtypes = [vp, dp, dp, dp]
-    L.dvqls_cost_batch.argtypes = [vp, ctypes.c_int, dp, dp, dp]
+    # the per-call host-buffer entry points take plain addresses (c_void_p from int): building a
+    # ctypes double pointer costs ~3 us per argument, a noticeable share of a K = 1 call
+    L.dvqls_cost.argtypes = [vp, vp, vp, vp]
+    L.dvqls_cost_batch.argtypes = [vp, ctypes.c_int, vp, vp, vp]
     L.dvqls_cost_dev.argtypes = [vp, ctypes.c_int, vp, vp]
     L.dvqls_terms_local_dev.argtypes = [vp, vp, vp]
     L.dvqls_state.argtypes = [vp, dp, dp]
@@ -258,6 +260,13 @@ class Context:
         _check(rc, None)
         self.h = h
         self.max_batch = max_batch
+        # per-call host buffers of the cost entry points, allocated once (their addresses cached)
+        self._th_buf = np.empty(max(1, max_batch) * self.P)
+        self._c_buf = np.empty(max(1, max_batch))
+        self._ep_buf = np.empty(4 * max(1, max_batch))
+        self._th_addr = self._th_buf.ctypes.data
+        self._c_addr = self._c_buf.ctypes.data
+        self._ep_addr = self._ep_buf.ctypes.data
 
     # --- host-buffer entry points --------------------------------------------
     def terms(self, theta) -> np.ndarray:
@@ -269,10 +278,13 @@ class Context:
 
     def cost(self, theta, with_E_Psi=False):
         th = self._theta(theta, 1)
-        c = np.empty(1)
-        ep = np.empty(4)
-        _check(load().dvqls_cost(self.h, _dp(th), _dp(c), _dp(ep)), self.h)
-        return (float(c[0]), complex(ep[0], ep[1]), complex(ep[2], ep[3])) if with_E_Psi else float(c[0])
+        self._th_buf[:self.P] = th
+        rc = _lib.dvqls_cost(self.h, self._th_addr, self._c_addr, self._ep_addr)
+        if rc:
+            _check(rc, self.h)
+        ep = self._ep_buf
+        return (float(self._c_buf[0]), complex(ep[0], ep[1]), complex(ep[2], ep[3])) if with_E_Psi \
+            else float(self._c_buf[0])
 
     def global_cost(self, theta, with_beta=False):
         """NEXT-3: (C_L, C_G, E, Psi[, beta]) of one theta (Eq. 1 and Alg. 1 forms)."""
@@ -291,10 +303,13 @@ class Context:
         th = np.ascontiguousarray(thetas, dtype=np.float64)
         K = th.shape[0]
         th = self._theta(th, K)
-        c = np.empty(K)
-        ep = np.empty(4 * K)
-        _check(load().dvqls_cost_batch(self.h, K, _dp(th), _dp(c), _dp(ep)), self.h)
-        return c, ep.reshape(K, 4)
+        if K > self.max_batch:  # the library rejects it: report through its error path
+            _check(load().dvqls_cost_batch(self.h, K, th.ctypes.data, self._c_addr, self._ep_addr), self.h)
+        self._th_buf[:K * self.P] = th
+        rc = _lib.dvqls_cost_batch(self.h, K, self._th_addr, self._c_addr, self._ep_addr)
+        if rc:
+            _check(rc, self.h)
+        return self._c_buf[:K].copy(), self._ep_buf[:4 * K].reshape(K, 4).copy()
 
     def cost_grad(self, theta, with_E_Psi=False):
         """Parameter-shift gradient (dvqls_cost_grad): (C, dC/dtheta[P]) [+ (E, Psi)]."""
