@@ -101,6 +101,28 @@ def test_batch_equals_single(dv):
         ctx.destroy()
 
 
+def test_host_buffer_calls_reuse_safely(dv):
+    """The binding's cost / cost_batch reuse one set of host buffers per context (and the library
+    its mapped pinned stage): interleaved calls with different K return independent arrays with
+    the oracle's values, and K > max_batch is an error, not a buffer overrun."""
+    w = configs.random_workload(6, 3, 2, seed=77)
+    ctx = dv.from_workload(w, max_batch=4)
+    try:
+        ths = np.stack([w.theta0(s) for s in range(4)])
+        ref = [ocost.cost(sim.workload_terms(w, t), ocost.coeffs_of(w), w.n, w.L)[0] for t in ths]
+        c4, e4 = ctx.cost_batch(ths)
+        c1 = ctx.cost(ths[2])
+        c2, _ = ctx.cost_batch(ths[:2])
+        assert np.max(np.abs(c4 - ref)) <= TOL and abs(c1 - ref[2]) <= TOL
+        assert np.array_equal(c2, c4[:2]) and c1 == c4[2]   # the first result was not overwritten
+        assert e4.shape == (4, 4)
+        with pytest.raises(dv.DvqlsError):
+            ctx.cost_batch(np.stack([w.theta0(s) for s in range(5)]))
+        assert ctx.cost(ths[0]) == c4[0]  # still usable after the rejected call
+    finally:
+        ctx.destroy()
+
+
 def test_deterministic_bitwise(dv):
     w = configs.cfg3()
     ctx = dv.from_workload(w)
