@@ -279,7 +279,7 @@ def measure_traffic(args, kernel):
                "-k", f"regex:{name}", "-s", "1", "-c", "1", "--log-file", log,
                sys.executable, os.path.abspath(__file__), *fwd, "--traffic-probe"]
         try:
-            r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=180)
             rows = list(csv.reader(open(log))) if os.path.exists(log) else []
         except (OSError, subprocess.SubprocessError) as e:
             return None, f"ncu capture failed: {type(e).__name__}"
