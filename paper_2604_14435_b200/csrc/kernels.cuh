@@ -291,7 +291,10 @@ prefix_lanes_kernel(int layers, int entangler, const double* __restrict__ thetas
 // phase timestamps for tools/prefix_timing.cu (compiled with -DDVQLS_PREFIX_TS; no code otherwise)
 #ifdef DVQLS_PREFIX_TS
 __device__ long long g_prefix_ts[256];
-#define PREFIX_TS(k) do { if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_prefix_ts[(threadIdx.x >> 5) * 16 + (k)] = clock64(); } while (0)
+__device__ unsigned long long g_prefix_gt[256];  // %globaltimer (ns) at the same stamps
+#define PREFIX_TS(k) do { if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) { \
+    unsigned long long gt_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_)); \
+    g_prefix_ts[(threadIdx.x >> 5) * 16 + (k)] = clock64(); g_prefix_gt[(threadIdx.x >> 5) * 16 + (k)] = gt_; } } while (0)
 #else
 #define PREFIX_TS(k) do { } while (0)
 #endif

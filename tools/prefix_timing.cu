@@ -8,6 +8,12 @@
 #include <cstdio>
 #include <vector>
 #include "kernels.cuh"
+__global__ void empty_kernel(double2* x) {
+  extern __shared__ double2 esm[];
+  if (threadIdx.x == 0) esm[0] = x[0];
+  __syncthreads();
+  if (threadIdx.x == 0) x[1] = esm[0];
+}
 int main() {
   const int n = 10, d = 10, P = 3 * n * d, N = 1 << n;
   std::vector<double> th(P);
@@ -40,6 +46,23 @@ int main() {
     for (int k = 1; k <= 4; ++k) printf("%s%lld", k > 1 ? ", " : "", ts[w * 16 + k] - ts[w * 16]);
     printf("]");
   }
-  printf("]}\n");
+  printf("]");
+  // the same kernel, stamped again once alone: %globaltimer duration of its body and the SM clock
+  dvqls::prefix_quad_kernel<10><<<1, N / 4, smem>>>(d, 0, dth, dx);
+  cudaDeviceSynchronize();
+  unsigned long long gt[256];
+  cudaMemcpyFromSymbol(ts, dvqls::g_prefix_ts, sizeof ts);
+  cudaMemcpyFromSymbol(gt, dvqls::g_prefix_gt, sizeof gt);
+  const double ns = double(gt[4] - gt[0]), cyc = double(ts[4] - ts[0]);
+  printf(", \"body_ns_warp0\": %.0f, \"body_cycles_warp0\": %.0f, \"sm_ghz_in_body\": %.3f", ns, cyc, cyc / ns);
+  // launch floor: an (almost) empty kernel with the same launch configuration, back to back
+  cudaFuncSetAttribute((const void*)&empty_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  for (int i = 0; i < 5; ++i) empty_kernel<<<1, N / 4, smem>>>(dx);
+  cudaEventRecord(e0);
+  for (int i = 0; i < 100; ++i) empty_kernel<<<1, N / 4, smem>>>(dx);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf(", \"empty_us_per_launch_back_to_back\": %.2f}\n", ms * 10.0f);
   return 0;
 }
